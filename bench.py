@@ -1,0 +1,289 @@
+"""Benchmark of the FED-FEM explicit step (BASELINE.json metric: element-steps/s,
+ms/step, % of HBM roofline).
+
+Default workload: BASELINE config 4 -- the >=10M-element temperature-dependent
+mesh named by north_star's roofline target (256^3 trilinear hexes, 16.8M
+elements, 16.97M nodes, TD k/c/perfusion, per-element log-normal conductivity
+factor, moving Gaussian source, Dirichlet 37 C on all faces, fp32), one fused
+step kernel per step.  ``--config cfg1|cfg2|cfg3`` selects another workload.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fast|reference]
+
+Timing: W warm-up steps, then K steps bracketed by a barrier +
+synchronize, CUDA events on the engine's stream, max over ranks.  The
+per-step input (1.1 GB of slot + node streams for cfg4) is larger than the
+126 MB L2, so no L2 flush is needed between steps.  ``e2e`` is the same metric
+through the public C ABI with host buffers (fh_step_host: pinned host T in,
+one step, host T out, every step).  ``--impl reference`` times the CPU oracle
+(restated reference path, oracle/fh_oracle.c, all host threads) on a bounded
+sample of the same workload family.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="fast", choices=["fast", "reference"])
+    ap.add_argument("--config", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--precision", type=int, default=0)
+    ap.add_argument("--divisions", type=int, default=0, help="override mesh divisions (testing)")
+    ap.add_argument("--part-nodes", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-div", type=int, default=0)
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def make_problem(name, divisions=0, precision=0):
+    from paper_1909_05098_b200 import configs
+
+    fn = getattr(configs, name)
+    kw = {}
+    if divisions:
+        kw["divisions"] = divisions
+    if precision and name in ("cfg2", "cfg3"):
+        kw["precision"] = precision
+    prob = fn(**kw)
+    if precision:
+        prob.precision = precision
+    return prob
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.samples = []
+        self.proc = None
+        self.index = index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu=timestamp,{self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        rows = [s for ts, s in self.samples if t0 - 0.05 <= ts <= t1 + 0.05] or [s for _, s in self.samples[-3:]]
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            parts = [p.strip() for p in r.split(",")]
+            try:
+                sm.append(float(parts[1]))
+                smax = max(smax, float(parts[2]))
+            except (ValueError, IndexError):
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_oracle_rate(name, divisions, steps, threads=None):
+    """Time the CPU oracle (restated reference path) on a bounded sample."""
+    from oracle import oracle as orc
+
+    prob = make_problem(name, divisions)
+    mesh = prob.mesh
+    from paper_1909_05098_b200.solver import resolve_boundary
+    from paper_1909_05098_b200.sources import robin_lumps
+
+    rb = resolve_boundary(prob.boundary, mesh)
+    robin = None
+    if prob.robin:
+        robin = robin_lumps(mesh, prob.robin[0], exclude=rb.dirichlet_nodes)
+    if threads:
+        orc.set_threads(threads)
+    ora = orc.OracleModel(mesh, prob.material, dirichlet=(rb.dirichlet_nodes, rb.dirichlet_values),
+                          sources=[s.as_dict() for s in prob.sources], robin=robin, kfactor=prob.kfactor,
+                          td_mode=prob.td_mode)
+    ora.initial_state(37.0)
+    dt = 0.9 * ora.critical_dt(np.full(mesh.n_nodes, 37.0))
+    ora.step(dt, 1)  # warm-up
+    t0 = time.perf_counter()
+    ora.step(dt, steps)
+    el = time.perf_counter() - t0
+    return mesh.n_elements * steps / el, el, mesh.n_elements, orc.max_threads()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    div = args.cpu_sample_div or {"cfg4": 96, "cfg3": 40, "cfg1": 20, "cfg2": 20}[args.config]
+    per_step = []
+    elem = 0
+    for i in range(args.warmup + args.steps):
+        rate, el, elem, threads = cpu_oracle_rate(args.config, div, 1)
+        if i >= args.warmup:
+            per_step.append(el)
+    tot = sum(per_step)
+    value = elem * len(per_step) / tot
+    sample = f"{args.config}-family mesh at {div}^3 cells ({elem} elements), one oracle step per bench step"
+    line = {
+        "impl": "reference", "metric": "element-steps/sec", "value": value, "unit": "element-steps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(per_step),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "sample_divisions": div},
+        "cpu_baseline": {"value": value, "unit": "element-steps/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "element-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+
+    import paper_1909_05098_b200 as fh
+    from paper_1909_05098_b200 import _native as N
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        raise SystemExit("multi-GPU bench: see bench_dist (not built in this revision)")
+    torch.cuda.set_device(local)
+    prob = make_problem(args.config, args.divisions, args.precision)
+    mesh = prob.mesh
+    t_setup = time.perf_counter()
+    eng = fh.ExplicitEngine(mesh, prob.material, prob.boundary, assembly="tiled", device=local,
+                            part_nodes=args.part_nodes, **prob.engine_kwargs())
+    t_setup = time.perf_counter() - t_setup
+    dt = 0.9 * eng.critical_dt(37.0)
+    if prob.name == "cfg4":  # moving source: traverse the seeded segment over the run
+        a, b = (np.asarray(v) for v in prob.notes["path"])
+        src = fh.GaussianSource(amp=5.0e6, sigma=0.005, x0=tuple(a), vel=tuple((b - a) / (prob.steps * dt)),
+                                t0=0.0)
+        eng.set_sources([src])
+    st = eng.initial_state(37.0)
+    import ctypes as C
+
+    L, h = eng._L, eng._h
+    T = st.temperatures
+    N.check(L.fh_set_temperature(h, N.ptr(T), T.size, 0, 0.0))
+    stream = torch.cuda.ExternalStream(eng.stream())
+    rep = N.FhReport()
+    N.check(L.fh_step(h, args.warmup, dt, C.byref(rep)))
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    wall0 = time.time()
+    elapsed = C.c_float(0.0)
+    # CUDA events recorded on the engine's launch stream around the K launches
+    rc = L.fh_step_timed(h, args.steps, dt, C.byref(rep), C.byref(elapsed))
+    torch.cuda.synchronize()
+    wall1 = time.time()
+    N.check(rc)
+    del stream
+    ms_total = float(elapsed.value)
+    time.sleep(0.15)
+    sampler.stop()
+    clocks = sampler.summary(wall0, wall1)
+    lay = eng.layout()
+    E = mesh.n_elements
+    ms = ms_total / args.steps
+    value = E * args.steps / (ms_total / 1e3)
+    peak, peak_kind = peaks()
+    achieved = lay["canonical_bytes"] / (ms / 1e3) / 1e9
+    # e2e: through the public C ABI with pinned host buffers, one step per call
+    Tin = torch.empty(mesh.n_nodes, dtype=torch.float64, pin_memory=True)
+    Tout = torch.empty(mesh.n_nodes, dtype=torch.float64, pin_memory=True)
+    Tin.numpy()[:] = T
+    p_in = C.cast(C.c_void_p(Tin.data_ptr()), N.f64p)
+    p_out = C.cast(C.c_void_p(Tout.data_ptr()), N.f64p)
+    N.check(L.fh_step_host(h, p_in, p_out, T.size, 1, dt, C.byref(rep)))
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        N.check(L.fh_step_host(h, p_in, p_out, T.size, 1, dt, C.byref(rep)))
+    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(args.config)
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0:
+        div = args.cpu_sample_div or {"cfg4": 96, "cfg3": 40, "cfg1": 20, "cfg2": 20}[args.config]
+        rate, el, elem, threads = cpu_oracle_rate(args.config, div, 3)
+        cpu = {"value": rate, "unit": "element-steps/s", "cores": threads, "kind": "port",
+               "sample": f"oracle (fh_oracle.c, fp64, reference op order) on the {args.config} family at {div}^3 "
+                         f"cells ({elem} elements), 3 steps after 1 warm-up"}
+    line = {
+        "metric": "element-steps/sec", "value": value, "unit": "element-steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if prob.precision == 32 else "f64",
+        "data": "synthetic (seeded, BASELINE.json shapes)",
+        "config": {"workload": prob.name, "elements": E, "nodes": mesh.n_nodes, "td": prob.td_mode,
+                   "assembly": "tiled", "parts": lay["n_parts"], "slots": lay["n_slots"],
+                   "l2": "per-step input > 126 MB L2 (no flush needed)", "dt_s": dt, "setup_s": t_setup},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_kind": peak_kind,
+                     "canonical_bytes_per_step": lay["canonical_bytes"], "layout_bytes_per_step": lay["step_bytes"]},
+        "cpu_baseline": cpu,
+        "e2e": {"value": E / e2e_s, "unit": "element-steps/s", "h2d_bytes_per_step": 8 * mesh.n_nodes,
+                "d2h_bytes_per_step": 8 * mesh.n_nodes},
+        "gpu_launches": args.steps * lay["kernels_per_step"],
+        "clocks": clocks,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,231 @@
+/*
+ * fedheat_b200.h -- C ABI of the B200-native FED-FEM bio-heat engine
+ * (libfedheat_b200.so).  Plain pointers and sizes only; no torch or CUDA
+ * types cross this boundary.  Host arrays are borrowed for the duration of a
+ * call; every device buffer is owned by the library.
+ *
+ * Two layers, each a drop-in for a layer of the reference package
+ * (/root/reference/pkg/src/fedheat/, cited file:line below):
+ *
+ *  1. Operator layer -- one entry point per numba kernel of kernels.py, same
+ *     argument meaning, caller-allocated outputs, bit-identical results.  A
+ *     maintainer swaps the numba bodies for these (INTEGRATION.md shows the
+ *     ctypes stub).  Each call copies its inputs to the GPU, runs one CUDA
+ *     kernel and copies the result back.
+ *
+ *  2. Engine layer -- the stateful step path of solver.ExplicitEngine
+ *     (solver.py:243-519): mesh/material/boundary upload and device
+ *     precompute in fh_create, device-resident stepping in fh_step.
+ *
+ * Status codes: 0 ok, 1 config error (ConfigError), 2 instability
+ * (InstabilityError), 3 CUDA/NCCL failure, 4 degenerate element
+ * (DegenerateElementError).  fh_last_error() returns the calling thread's
+ * message for the last non-zero status.
+ */
+#ifndef FEDHEAT_B200_H
+#define FEDHEAT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FH_OK 0
+#define FH_ERR_CONFIG 1
+#define FH_ERR_INSTABILITY 2
+#define FH_ERR_DEVICE 3
+#define FH_ERR_DEGENERATE 4
+
+#define FH_MAX_KNOTS 32
+#define FH_CHUNK_SIZE 4096 /* solver.py:48 CHUNK_SIZE */
+
+const char *fh_last_error(void);
+int fh_version(void);
+int fh_device_count(int *count);
+
+/* ------------------------------------------------------------------ */
+/* 1. Operator layer (kernels.py:76-142).  All arrays are host memory. */
+/* ------------------------------------------------------------------ */
+
+/* kernels.py:76-79 eval_curve_nodes(xs, ys, temps, out) */
+int fh_eval_curve_nodes(const double *xs, const double *ys, int64_t n_knots, const double *temps,
+                        int64_t n, double *out);
+
+/* kernels.py:82-86 lumped_capacity_nodes(rho_x, rho_y, c_x, c_y, temps, vols, out) */
+int fh_lumped_capacity_nodes(const double *rho_x, const double *rho_y, int64_t n_rho, const double *c_x,
+                             const double *c_y, int64_t n_c, const double *temps, const double *vols,
+                             int64_t n, double *out);
+
+/* kernels.py:89-98 element_mean_nodal(conn_data, conn_offs, nodal, out) */
+int fh_element_mean_nodal(const int64_t *conn_data, const int64_t *conn_offs, int64_t n_elem,
+                          const double *nodal, int64_t n_nodes, double *out);
+
+/* kernels.py:101-134 scatter_net_loads(conn_data, conn_offs, mat_data, mat_offs, kbar, temps,
+ * n_chunks, chunk_size, buffers, out) -- the O(n_chunks * n_nodes) `buffers`
+ * scratch of the reference is not needed; the chunk semantics (private
+ * partial per chunk_size elements, partials added in chunk order) are kept. */
+int fh_scatter_net_loads(const int64_t *conn_data, const int64_t *conn_offs, const double *mat_data,
+                         const int64_t *mat_offs, int64_t n_elem, const double *kbar, const double *temps,
+                         int64_t n_nodes, int64_t chunk_size, double *out);
+
+/* kernels.py:137-142 nodal_update(temps, inflow, capacity, perf_k, perf_q, metab_q, extra_q, dt);
+ * temps is updated in place. */
+int fh_nodal_update(double *temps, const double *inflow, const double *capacity, const double *perf_k,
+                    const double *perf_q, const double *metab_q, const double *extra_q, int64_t n,
+                    double dt);
+
+/* ------------------------------------------------------------------ */
+/* 2. Engine layer (solver.py:243-519)                                  */
+/* ------------------------------------------------------------------ */
+
+typedef struct fh_engine fh_engine;
+
+typedef struct {
+  int32_t n; /* knots, 1..FH_MAX_KNOTS; 0 = absent (only for `perfusion`) */
+  const double *x;
+  const double *y;
+} fh_curve;
+
+/* material.py:65-123 TissueMaterial; `perfusion` (extension) makes the
+ * perfusion rate temperature dependent and replaces perfusion_rate. */
+typedef struct {
+  fh_curve density, specific_heat, conductivity, perfusion;
+  double perfusion_rate, blood_specific_heat, arterial_temperature, metabolic_rate;
+} fh_material;
+
+/* mesh.py:38-59 Mesh: nodes (V,3) float64, tets (Et,4), hexes (Eh,8) int64;
+ * global element order = tets then hexes. */
+typedef struct {
+  int64_t n_nodes;
+  const double *coords;
+  int64_t n_tets;
+  const int64_t *tets;
+  int64_t n_hexes;
+  const int64_t *hexes;
+} fh_mesh;
+
+#define FH_SOURCE_GAUSSIAN 0 /* amp * exp(-|x - c(t)|^2 / (2 sigma^2)), c(t) = x0 + vel * t */
+#define FH_SOURCE_RF 1       /* min(amp / (4 pi |x - x0|^2), cap) */
+typedef struct {
+  int32_t kind;
+  double amp, sigma, cap;
+  double x0[3], vel[3];
+  double t0, t1; /* active while t0 <= t < t1 (t = step start time) */
+} fh_source;
+
+/* solver.py:91-164 BoundarySpec after resolve_boundary, plus extensions. */
+typedef struct {
+  int64_t n_dirichlet; /* sorted unique node ids, values */
+  const int64_t *dirichlet_nodes;
+  const double *dirichlet_values;
+  int64_t n_loads; /* heat_loads: nodes of load l are load_nodes[load_offsets[l]:load_offsets[l+1]] */
+  const int64_t *load_offsets;
+  const int64_t *load_nodes;
+  const double *load_power, *load_t0, *load_t1;
+  const double *q_static; /* extension: (V,) static nodal power in W, or NULL */
+  int32_t n_sources;      /* extension: volumetric sources lumped as Q(x_i, t) * v_i */
+  const fh_source *sources;
+  int64_t n_robin; /* extension: convective nodes, rate += hA*(Tinf) - hA*T */
+  const int64_t *robin_nodes;
+  const double *robin_hA, *robin_hAT;
+} fh_boundary;
+
+#define FH_ASSEMBLY_EXACT 0  /* fp64, reference operation order, bitwise == reference */
+#define FH_ASSEMBLY_TILED 1  /* fused owner-computes tiles, G-form, deterministic */
+#define FH_ASSEMBLY_ATOMIC 2 /* element kernel + red.global into F, then node update (tolerance only) */
+
+typedef struct {
+  int32_t precision; /* 64 or 32 (32 only for TILED / ATOMIC) */
+  int32_t assembly;
+  int32_t td_mode;   /* 1: refresh properties every step; 0: freeze at first step */
+  int32_t device;    /* CUDA ordinal */
+  double runaway_limit;
+  int32_t n_materials; /* >= 1; >1 = regions (extension) */
+  const fh_material *materials;
+  const int32_t *element_region;  /* (E,) or NULL */
+  const double *element_kfactor;  /* (E,) or NULL: extension, kbar_e *= f_e */
+  int32_t part_nodes;             /* TILED: nodes per tile (0 = default) */
+  int32_t n_domains;              /* multi-GPU: domains the mesh is cut into (1, 2, 4 or 8) */
+  int32_t domain_lo, domain_hi;   /* this engine owns domains [lo, hi) */
+  int32_t slab_axis;              /* -1: recursive coordinate bisection; 0/1/2: domains are slabs */
+} fh_options;
+
+typedef struct {
+  int64_t steps_done;
+  int64_t fail_step; /* -1 if none */
+  int64_t fail_node; /* original numbering; -1 if none */
+  double fail_value;
+  double time;       /* state time after the call */
+  int64_t step_index;
+} fh_report;
+
+int fh_create(const fh_mesh *mesh, const fh_boundary *boundary, const fh_options *opts, fh_engine **out);
+int fh_destroy(fh_engine *e);
+
+/* state (original node numbering, float64 on the host side) */
+int fh_set_temperature(fh_engine *e, const double *T, int64_t n, int64_t step_index, double time);
+int fh_get_temperature(fh_engine *e, double *T, int64_t n);
+int fh_get_inflow(fh_engine *e, double *F, int64_t n); /* EXACT: last step's F */
+int fh_reset_properties(fh_engine *e);                 /* next step refreshes (TI re-freeze) */
+
+/* advance nsteps explicit steps of size dt (solver.py:348-382 each).  If
+ * probes were set, T[probe] is recorded after every step whose new index is
+ * a multiple of the probe interval.  Returns FH_ERR_INSTABILITY with the
+ * report filled when a step produced a non-finite or runaway temperature; the
+ * state is then the one right after that step. */
+int fh_step(fh_engine *e, int64_t nsteps, double dt, fh_report *rep);
+
+/* fh_step with CUDA events recorded on the engine's stream around the
+ * launches; *elapsed_ms = device time of the nsteps steps. */
+int fh_step_timed(fh_engine *e, int64_t nsteps, double dt, fh_report *rep, float *elapsed_ms);
+
+/* same, with host I/O around it: upload T_in (n doubles), step, download
+ * the new field into T_out -- the reference's ExplicitEngine.step contract
+ * with host-resident state (used for the e2e measurement). */
+int fh_step_host(fh_engine *e, const double *T_in, double *T_out, int64_t n, int64_t nsteps, double dt,
+                 fh_report *rep);
+
+/* replace the time-dependent volumetric sources (n <= 8) after creation */
+int fh_set_sources(fh_engine *e, const fh_source *sources, int32_t n);
+
+int fh_set_probes(fh_engine *e, const int64_t *nodes, int64_t n, int64_t interval, int64_t capacity);
+int fh_get_probes(fh_engine *e, double *values, int64_t max_records, int64_t *n_records);
+
+/* solver.py:384-405 Gershgorin bound 2/lambda_hat at field T (NULL = current
+ * state); bitwise == reference in EXACT mode. */
+int fh_critical_dt(fh_engine *e, const double *T, int64_t n, double *out);
+
+/* solver.py:223-240 scatter_loads with a given kbar (EXACT mode only). */
+int fh_scatter_loads(fh_engine *e, const double *kbar, const double *T, int64_t n, double *out);
+
+/* precompute results (original numbering): lumped node volumes (V) and
+ * element volumes (E). */
+int fh_get_precompute(fh_engine *e, double *node_volumes, double *elem_volumes);
+
+/* layout facts for the roofline: bytes the step kernel streams per step and
+ * counts. */
+typedef struct {
+  int64_t n_parts, n_slots, n_nodes_owned, n_elements;
+  int64_t step_bytes;      /* bytes the fused step streams from/to HBM (layout) */
+  int64_t canonical_bytes; /* SURVEY 8(d) canonical bytes per step */
+  int32_t kernels_per_step;
+  int32_t max_part_nodes;
+} fh_layout;
+int fh_get_layout(fh_engine *e, fh_layout *out);
+
+/* raw stream handle (cudaStream_t as void*) for CUDA-event timing from the host */
+void *fh_stream(fh_engine *e);
+
+/* permutation new->original node ids (TILED), for bookkeeping tests */
+int fh_get_node_order(fh_engine *e, int64_t *new_to_old, int64_t n);
+
+/* multi-GPU: NCCL bootstrap.  Rank 0 creates the id (128 bytes), the
+ * caller broadcasts it (torch.distributed), every rank attaches. */
+int fh_nccl_unique_id(char *id128);
+int fh_attach_nccl(fh_engine *e, const char *id128, int32_t rank, int32_t world);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

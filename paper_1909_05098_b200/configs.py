@@ -1,0 +1,95 @@
+"""The BASELINE.json workloads as seeded synthetic problems.
+
+Builder decisions for the parameters BASELINE leaves open are documented in
+DESIGN.md "Open parameters"; everything is seeded so the GPU engine, the oracle
+and the CPU baseline see identical inputs.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .material import TissueMaterial, linear_law, make_constant
+from .meshgen import generate_cube_mesh, jittered_cube_mesh
+from .solver import BoundarySpec
+from .sources import GaussianSource, RobinSpec
+
+FACES = ("x0", "x1", "y0", "y1", "z0", "z1")
+PERFUSION_SLOPE = 0.002  # 1/K, open parameter
+
+
+@dataclass
+class Problem:
+    name: str
+    mesh: object
+    material: TissueMaterial
+    boundary: BoundarySpec
+    steps: int
+    precision: int
+    td_mode: bool
+    sources: tuple = ()
+    robin: tuple = ()
+    kfactor: np.ndarray | None = None
+    auto_dt_safety: float = 0.9
+    notes: dict = field(default_factory=dict)
+
+    def engine_kwargs(self):
+        return dict(td_mode=self.td_mode, precision=self.precision, sources=self.sources, robin=self.robin,
+                    kfactor=self.kfactor)
+
+
+def pennes_constant() -> TissueMaterial:
+    # BASELINE cfg1: rho 1060, c 3600, k 0.5; w_b = 0.5e-3 1/s * rho_b 1050 -> 0.525 kg/(m^3 s)
+    return TissueMaterial.constant(density=1060.0, specific_heat=3600.0, conductivity=0.5, perfusion_rate=0.525,
+                                   blood_specific_heat=3640.0, arterial_temperature=37.0, metabolic_rate=420.0)
+
+
+def pennes_td(perfusion_td: bool = True, k0: float = 0.5, wb0: float = 0.525) -> TissueMaterial:
+    # BASELINE cfg2 laws: k = 0.5 (1 + 0.0013 (T-37)), c = 3600 (1 - 0.0005 (T-37)), rho const,
+    # perfusion linear in T (slope = PERFUSION_SLOPE, open parameter)
+    return TissueMaterial(
+        density=make_constant(1060.0), specific_heat=linear_law(3600.0, -0.0005, 37.0),
+        conductivity=linear_law(k0, 0.0013, 37.0), perfusion_rate=wb0, blood_specific_heat=3640.0,
+        arterial_temperature=37.0, metabolic_rate=420.0,
+        perfusion_curve=linear_law(wb0, PERFUSION_SLOPE, 37.0) if perfusion_td else None)
+
+
+def cfg1(divisions: int = 20) -> Problem:
+    mesh = generate_cube_mesh("hex", divisions, 0.1)
+    src = GaussianSource(amp=5.0e6, sigma=0.005, x0=(0.05, 0.05, 0.05))
+    return Problem("cfg1", mesh, pennes_constant(), BoundarySpec(dirichlet=tuple((f, 37.0) for f in FACES)),
+                   steps=1000, precision=64, td_mode=False, sources=(src,))
+
+
+def cfg2(divisions: int = 20, precision: int = 64) -> Problem:
+    mesh = generate_cube_mesh("hex", divisions, 0.1)
+    src = GaussianSource(amp=2.0e7, sigma=0.005, x0=(0.05, 0.05, 0.05))
+    return Problem("cfg2", mesh, pennes_td(), BoundarySpec(dirichlet=tuple((f, 37.0) for f in FACES)),
+                   steps=2000, precision=precision, td_mode=True, sources=(src,))
+
+
+def cfg3(divisions: int = 100, precision: int = 32, seed: int = 3) -> Problem:
+    mesh = jittered_cube_mesh("tet", divisions, 0.1, 0.2, seed=seed)
+    rng = np.random.default_rng(seed + 1000)
+    centres = rng.uniform(0.025, 0.075, (3, 3))
+    srcs = tuple(GaussianSource(amp=5.0e6, sigma=0.005, x0=tuple(c)) for c in centres)
+    bnd = BoundarySpec(dirichlet=tuple((f, 37.0) for f in FACES if f != "z1"))
+    return Problem("cfg3", mesh, pennes_td(), bnd, steps=500, precision=precision, td_mode=True, sources=srcs,
+                   robin=(RobinSpec("z1", 10.0, 25.0),))
+
+
+def cfg4(divisions: int = 256, seed: int = 4) -> Problem:
+    mesh = generate_cube_mesh("hex", divisions, 0.1)
+    rng = np.random.default_rng(seed)
+    # per-element log-normal conductivity factor, sigma 0.2, median 1 (open parameter: normalisation)
+    kf = np.exp(0.2 * rng.standard_normal(mesh.n_elements))
+    a, b = rng.uniform(0.03, 0.07, 3), rng.uniform(0.03, 0.07, 3)
+    steps = 200
+    # moving source: straight segment a -> b traversed over the run at constant speed
+    vel = tuple((b - a) / (steps * 1.0))  # m/s for dt = 1 s; rescaled in the bench to the actual dt
+    src = GaussianSource(amp=5.0e6, sigma=0.005, x0=tuple(a), vel=vel)
+    bnd = BoundarySpec(dirichlet=tuple((f, 37.0) for f in FACES))
+    return Problem("cfg4", mesh, pennes_td(), bnd, steps=steps, precision=32, td_mode=True, sources=(src,),
+                   kfactor=kf, notes={"path": (a.tolist(), b.tolist())})

@@ -1,0 +1,1264 @@
+// C ABI of libfedheat_b200.so (include/fedheat_b200.h): engine lifetime,
+// device precompute, state I/O, stepping, probes, critical dt, operator layer.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <type_traits>
+
+#include "fh_tiled.cuh"
+
+using namespace fh;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int report(const std::exception &ex) {
+  if (const auto *fe = dynamic_cast<const Error *>(&ex)) {
+    g_last_error = fe->what();
+    return fe->code;
+  }
+  g_last_error = ex.what();
+  return FH_ERR_DEVICE;
+}
+
+#define FH_API_BEGIN try {
+#define FH_API_END                   \
+  }                                  \
+  catch (const std::exception &ex) { \
+    return report(ex);               \
+  }                                  \
+  return FH_OK;
+
+template <typename S>
+void fill_curve(Curve<S> &c, const fh_curve &src, const char *what, bool optional = false) {
+  std::memset(&c, 0, sizeof(c));
+  if (src.n == 0 && optional) return;
+  if (src.n < 1 || src.n > FH_MAX_KNOTS)
+    fail(FH_ERR_CONFIG, std::string(what) + ": curve needs 1.." + std::to_string(FH_MAX_KNOTS) + " knots");
+  c.n = src.n;
+  for (int j = 0; j < src.n; ++j) {
+    c.x[j] = (S)src.x[j];
+    c.y[j] = (S)src.y[j];
+    if (j + 1 < src.n) {
+      if (!(src.x[j + 1] > src.x[j])) fail(FH_ERR_CONFIG, std::string(what) + ": knots must increase");
+      c.slope[j] = (S)((src.y[j + 1] - src.y[j]) / (src.x[j + 1] - src.x[j]));
+    }
+  }
+}
+
+template <typename S>
+void fill_mats(MatSet<S> &ms, const fh_options &o) {
+  std::memset(&ms, 0, sizeof(ms));
+  if (o.n_materials < 1 || o.n_materials > kMaxRegions || !o.materials)
+    fail(FH_ERR_CONFIG, "need 1.." + std::to_string(kMaxRegions) + " materials");
+  ms.n = o.n_materials;
+  for (int r = 0; r < o.n_materials; ++r) {
+    const fh_material &m = o.materials[r];
+    Mat<S> &d = ms.m[r];
+    fill_curve(d.rho, m.density, "density");
+    fill_curve(d.c, m.specific_heat, "specific_heat");
+    fill_curve(d.k, m.conductivity, "conductivity");
+    fill_curve(d.wb, m.perfusion, "perfusion", true);
+    d.td_perf = m.perfusion.n > 0;
+    d.wbcb = (S)(m.perfusion_rate * m.blood_specific_heat);
+    d.cb = (S)m.blood_specific_heat;
+    d.Ta = (S)m.arterial_temperature;
+    d.Qm = (S)m.metabolic_rate;
+  }
+}
+
+__global__ void k_to_new(const double *__restrict__ src_old, const int64_t *__restrict__ old_of_new, int64_t V,
+                         float *__restrict__ df, double *__restrict__ dd, float *__restrict__ df2,
+                         double *__restrict__ dd2) {
+  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (n >= V) return;
+  const double v = src_old[old_of_new ? old_of_new[n] : n];
+  if (df) df[n] = (float)v;
+  if (dd) dd[n] = v;
+  if (df2) df2[n] = (float)v;
+  if (dd2) dd2[n] = v;
+}
+
+template <typename S>
+__global__ void k_to_old(const S *__restrict__ src_new, const int64_t *__restrict__ new_of_old, int64_t V,
+                         double *__restrict__ dst_old) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < V) dst_old[i] = (double)src_new[new_of_old ? new_of_old[i] : i];
+}
+
+template <typename S>
+__global__ void k_xyz_to_new(const double *__restrict__ xyz, const int64_t *__restrict__ old_of_new, int64_t V,
+                             S *__restrict__ out) {
+  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (n >= V) return;
+  const int64_t o = old_of_new[n];
+  out[3 * n] = (S)xyz[3 * o];
+  out[3 * n + 1] = (S)xyz[3 * o + 1];
+  out[3 * n + 2] = (S)xyz[3 * o + 2];
+}
+
+template <typename S>
+__global__ void k_pack_slots(const int32_t *__restrict__ slot_elem, int64_t n, const double *__restrict__ G,
+                             double scale, S *__restrict__ out_G, const double *__restrict__ kf,
+                             S *__restrict__ out_kf, const int32_t *__restrict__ region,
+                             uint8_t *__restrict__ out_region) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int64_t e = slot_elem[s];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) out_G[6 * s + k] = (S)(G[6 * e + k] * scale);
+  if (out_kf) out_kf[s] = (S)kf[e];
+  if (out_region) out_region[s] = (uint8_t)region[e];
+}
+
+constexpr int kBlk = 256;
+inline unsigned nblk(int64_t n) { return (unsigned)((n + kBlk - 1) / kBlk); }
+
+template <typename S>
+struct TiledState {
+  TiledArgs<S> args{};
+  DBuf<int32_t> part_node_start, part_n_free, part_robin_start, part_robin_base, part_tet_start, part_hex_start;
+  DBuf<int32_t> part_list;
+  DBuf<int32_t> tet_conn, hex_conn, tet_slot_elem, hex_slot_elem;
+  DBuf<S> tet_G, hex_G, tet_kf, hex_kf, tet_kbar, hex_kbar;
+  DBuf<uint8_t> tet_rank, hex_rank, tet_region, hex_region, node_region;
+  DBuf<S> T[2], vol, cap, kb, q_ext, xyz, robin_hA, robin_hAT;
+  int cur = 0;
+  size_t smem = 0;
+  int n_parts_local = 0;
+};
+
+}  // namespace
+
+struct fh_engine {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int precision = 64, assembly = FH_ASSEMBLY_EXACT;
+  bool td = false;
+  int64_t V = 0, E = 0, n_tet = 0, n_hex = 0, nconn = 0;
+  double runaway_limit = 1e6;
+  int64_t step_index = 0;
+  double time = 0.0;
+  bool frozen = false;
+  fh_options opts{};
+  MatSet<double> mats_d{};
+  MatSet<float> mats_f{};
+  // boundary (host)
+  std::vector<int64_t> dir_nodes;
+  std::vector<double> dir_vals;
+  std::vector<int64_t> load_offs, load_nodes;
+  std::vector<double> load_power, load_t0, load_t1;
+  std::vector<uint8_t> load_sig;
+  bool qr_valid = false;
+  std::vector<double> q_static;
+  std::vector<fh_source> sources;
+  std::vector<int64_t> robin_nodes;
+  std::vector<double> robin_hA, robin_hAT;
+  std::vector<double> host_xyz;
+  // common device data (original numbering)
+  DBuf<double> xyz, node_vol, elem_vol, row_abs, stage, stage2;
+  DBuf<int32_t> conn, csr_offs, csr_pos, elem_region, node_region;
+  DBuf<double> kfactor;
+  DBuf<FailFlag> flag;
+  // exact
+  ExactArgs ex{};
+  DBuf<double> A, kbar, cap, kb, qb, qm, qr, qstat, contrib, F, T, dir_vals_d, robin_hA_d, robin_hAT_d;
+  DBuf<int32_t> dir_slot, robin_slot;
+  // tiled
+  Partition part;
+  DBuf<int64_t> old_of_new, new_of_old;
+  std::unique_ptr<TiledState<float>> tf;
+  std::unique_ptr<TiledState<double>> tdd;
+  // probes
+  DBuf<int32_t> probes;
+  int64_t n_probes = 0, probe_interval = 1, probe_cap = 0, n_rec = 0;
+  DBuf<double> probe_hist;
+  std::vector<int64_t> probe_steps;
+  // critical dt scratch
+  DBuf<double> crit_kbar, crit_lam;
+
+  ~fh_engine() {
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+void check_engine(fh_engine *e) {
+  if (!e) fail(FH_ERR_CONFIG, "null engine");
+  FH_CUDA(cudaSetDevice(e->device));
+}
+
+// q_r from the active heat loads (solver.py:307-318) + static nodal power
+bool loads_changed(fh_engine *e, double t) {
+  const int64_t nl = (int64_t)e->load_power.size();
+  bool changed = !e->qr_valid;
+  for (int64_t l = 0; l < nl; ++l) {
+    const uint8_t on = (e->load_t0[l] <= t && t < e->load_t1[l]);
+    if (on != e->load_sig[l]) changed = true;
+    e->load_sig[l] = on;
+  }
+  e->qr_valid = true;
+  return changed;
+}
+
+std::vector<double> dense_qr(fh_engine *e) {
+  std::vector<double> qr(e->V, 0.0);
+  for (size_t l = 0; l < e->load_power.size(); ++l)
+    if (e->load_sig[l])
+      for (int64_t q = e->load_offs[l]; q < e->load_offs[l + 1]; ++q) qr[e->load_nodes[q]] += e->load_power[l];
+  return qr;
+}
+
+template <typename S>
+TiledState<S> &tstate(fh_engine *e);
+template <>
+TiledState<float> &tstate<float>(fh_engine *e) { return *e->tf; }
+template <>
+TiledState<double> &tstate<double>(fh_engine *e) { return *e->tdd; }
+
+template <typename S>
+MatSet<S> &mats_of(fh_engine *e);
+template <>
+MatSet<float> &mats_of<float>(fh_engine *e) { return e->mats_f; }
+template <>
+MatSet<double> &mats_of<double>(fh_engine *e) { return e->mats_d; }
+
+void upload_qr(fh_engine *e, double t) {
+  if (e->load_power.empty()) return;
+  if (!loads_changed(e, t)) return;
+  std::vector<double> qr = dense_qr(e);
+  FH_CUDA(cudaStreamSynchronize(e->stream));
+  if (e->assembly == FH_ASSEMBLY_EXACT) {
+    FH_CUDA(cudaMemcpy(e->qr.p, qr.data(), sizeof(double) * e->V, cudaMemcpyHostToDevice));
+    return;
+  }
+  if (!e->q_static.empty())
+    for (int64_t i = 0; i < e->V; ++i) qr[i] += e->q_static[i];
+  FH_CUDA(cudaMemcpy(e->stage.p, qr.data(), sizeof(double) * e->V, cudaMemcpyHostToDevice));
+  if (e->precision == 32)
+    k_to_new<<<nblk(e->V), kBlk>>>(e->stage.p, e->old_of_new.p, e->V, e->tf->q_ext.p, nullptr, nullptr, nullptr);
+  else
+    k_to_new<<<nblk(e->V), kBlk>>>(e->stage.p, e->old_of_new.p, e->V, nullptr, e->tdd->q_ext.p, nullptr, nullptr);
+  FH_CUDA(cudaGetLastError());
+  FH_CUDA(cudaDeviceSynchronize());
+}
+
+// ---------------------------------------------------------------------------
+void setup_exact(fh_engine *e, const fh_boundary &b) {
+  cudaStream_t s = e->stream;
+  const int64_t V = e->V;
+  ExactArgs &g = e->ex;
+  std::memset(&g, 0, sizeof(g));
+  g.V = V;
+  g.E = e->E;
+  g.n_tet = e->n_tet;
+  g.chunk_size = FH_CHUNK_SIZE;
+  g.conn = e->conn.p;
+  g.mat = e->A.p;
+  g.row_abs = e->row_abs.p;
+  g.csr_offs = e->csr_offs.p;
+  g.csr_pos = e->csr_pos.p;
+  g.node_vol = e->node_vol.p;
+  g.elem_region = e->elem_region.p;
+  g.node_region = e->node_region.p;
+  g.kfactor = e->kfactor.p;
+  g.mats = e->mats_d;
+  e->kbar.alloc(e->E);
+  e->cap.alloc(V);
+  e->contrib.alloc(e->nconn);
+  e->F.alloc(V);
+  e->F.zero(s);
+  e->T.alloc(V);
+  e->qr.alloc(V);
+  e->qr.zero(s);
+  g.kbar = e->kbar.p;
+  g.cap = e->cap.p;
+  g.contrib = e->contrib.p;
+  g.F = e->F.p;
+  g.qr = e->qr.p;
+  // constant lumps (precompute.py:43-53): kb = (wb*cb)*v, qb = kb*Ta, qm = Qm*v
+  std::vector<double> nv(V), kbh(V), qbh(V), qmh(V);
+  FH_CUDA(cudaMemcpyAsync(nv.data(), e->node_vol.p, sizeof(double) * V, cudaMemcpyDeviceToHost, s));
+  std::vector<int32_t> nreg(V, 0);
+  if (e->node_region.p)
+    FH_CUDA(cudaMemcpyAsync(nreg.data(), e->node_region.p, sizeof(int32_t) * V, cudaMemcpyDeviceToHost, s));
+  FH_CUDA(cudaStreamSynchronize(s));
+  for (int64_t i = 0; i < V; ++i) {
+    const fh_material &m = e->opts.materials[nreg[i]];
+    kbh[i] = (m.perfusion_rate * m.blood_specific_heat) * nv[i];
+    qbh[i] = kbh[i] * m.arterial_temperature;
+    qmh[i] = m.metabolic_rate * nv[i];
+  }
+  e->kb.upload(kbh, s);
+  e->qb.upload(qbh, s);
+  e->qm.upload(qmh, s);
+  g.kb = e->kb.p;
+  g.qb = e->qb.p;
+  g.qm = e->qm.p;
+  if (!e->q_static.empty()) {
+    e->qstat.upload(e->q_static, s);
+    g.q_static = e->qstat.p;
+  }
+  std::vector<int32_t> ds(V, -1);
+  for (size_t q = 0; q < e->dir_nodes.size(); ++q) ds[e->dir_nodes[q]] = (int32_t)q;
+  if (!e->dir_nodes.empty()) {
+    e->dir_slot.upload(ds, s);
+    e->dir_vals_d.upload(e->dir_vals, s);
+    g.dir_slot = e->dir_slot.p;
+    g.dir_vals = e->dir_vals_d.p;
+  }
+  if (!e->robin_nodes.empty()) {
+    std::vector<int32_t> rs(V, -1);
+    for (size_t q = 0; q < e->robin_nodes.size(); ++q) rs[e->robin_nodes[q]] = (int32_t)q;
+    e->robin_slot.upload(rs, s);
+    e->robin_hA_d.upload(e->robin_hA, s);
+    e->robin_hAT_d.upload(e->robin_hAT, s);
+    g.robin_slot = e->robin_slot.p;
+    g.robin_hA = e->robin_hA_d.p;
+    g.robin_hAT = e->robin_hAT_d.p;
+  }
+  g.xyz = e->xyz.p;
+  g.n_src = (int)e->sources.size();
+  for (int k = 0; k < g.n_src; ++k) g.src[k] = e->sources[k];
+  g.runaway_limit = e->runaway_limit;
+  g.flag = e->flag.p;
+  FH_CUDA(cudaStreamSynchronize(s));
+}
+
+// ---------------------------------------------------------------------------
+template <typename S>
+void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const double *G_dev) {
+  cudaStream_t s = e->stream;
+  const int64_t V = e->V;
+  const fh_options &o = e->opts;
+  // node classes
+  std::vector<uint8_t> cls(V, 0);
+  for (int64_t i : e->robin_nodes) cls[i] = 1;
+  for (int64_t i : e->dir_nodes) cls[i] = 2;
+  PartitionInput pin{};
+  pin.V = V;
+  pin.n_tet = e->n_tet;
+  pin.n_hex = e->n_hex;
+  pin.xyz = mesh.coords;
+  pin.tets = mesh.tets;
+  pin.hexes = mesh.hexes;
+  pin.node_class = cls.data();
+  pin.target_part_nodes = o.part_nodes > 0 ? o.part_nodes : (sizeof(S) == 4 ? 8192 : 4096);
+  pin.batch = kTileThreads;
+  pin.n_domains = std::max(1, o.n_domains);
+  pin.slab_axis = o.slab_axis;
+  build_partition(pin, e->part);
+  Partition &P = e->part;
+  e->old_of_new.upload(P.old_of_new, s);
+  e->new_of_old.upload(P.new_of_old, s);
+
+  auto st = std::make_unique<TiledState<S>>();
+  TiledArgs<S> &g = st->args;
+  std::memset(&g, 0, sizeof(g));
+  // parts of this engine: domains [lo, hi)
+  const int dlo = std::max(0, o.domain_lo), dhi = o.domain_hi > 0 ? o.domain_hi : pin.n_domains;
+  const int p_lo = P.domain_part_start[dlo], p_hi = P.domain_part_start[dhi];
+  std::vector<int32_t> plist;
+  for (int p = p_lo; p < p_hi; ++p) plist.push_back(p);
+  st->n_parts_local = (int)plist.size();
+  st->part_list.upload(plist, s);
+  std::vector<int32_t> robin_base(P.n_parts + 1, 0);
+  for (int p = 0; p < P.n_parts; ++p) robin_base[p + 1] = robin_base[p] + (P.part_n_free[p] - P.part_robin_start[p]);
+  st->part_node_start.upload(P.part_node_start, s);
+  st->part_n_free.upload(P.part_n_free, s);
+  st->part_robin_start.upload(P.part_robin_start, s);
+  st->part_robin_base.upload(robin_base, s);
+  st->part_tet_start.upload(P.part_tet_start, s);
+  st->part_hex_start.upload(P.part_hex_start, s);
+  st->tet_conn.upload(P.tet_conn, s);
+  st->hex_conn.upload(P.hex_conn, s);
+  st->tet_slot_elem.upload(P.tet_slot_elem, s);
+  st->hex_slot_elem.upload(P.hex_slot_elem, s);
+  if (!P.corner_unique) {
+    st->tet_rank.upload(P.tet_rank, s);
+    st->hex_rank.upload(P.hex_rank, s);
+  }
+  const int64_t nts = (int64_t)P.tet_slot_elem.size(), nhs = (int64_t)P.hex_slot_elem.size();
+  st->tet_G.alloc(6 * nts);
+  st->hex_G.alloc(6 * nhs);
+  const bool regions = o.n_materials > 1 && o.element_region;
+  if (e->kfactor.p) {
+    st->tet_kf.alloc(nts);
+    st->hex_kf.alloc(nhs);
+  }
+  if (regions) {
+    st->tet_region.alloc(nts);
+    st->hex_region.alloc(nhs);
+  }
+  if (nts)
+    k_pack_slots<S><<<nblk(nts), kBlk, 0, s>>>(st->tet_slot_elem.p, nts, G_dev, 1.0, st->tet_G.p, e->kfactor.p,
+                                               st->tet_kf.p, e->elem_region.p, st->tet_region.p);
+  if (nhs)
+    k_pack_slots<S><<<nblk(nhs), kBlk, 0, s>>>(st->hex_slot_elem.p, nhs, G_dev, 1.0 / 64.0, st->hex_G.p,
+                                               e->kfactor.p, st->hex_kf.p, e->elem_region.p, st->hex_region.p);
+  FH_CUDA(cudaGetLastError());
+  // nodal arrays in the new numbering
+  st->T[0].alloc(V);
+  st->T[1].alloc(V);
+  st->vol.alloc(V);
+  {
+    float *vf = nullptr;
+    double *vd = nullptr;
+    if constexpr (sizeof(S) == 4) vf = st->vol.p; else vd = st->vol.p;
+    k_to_new<<<nblk(V), kBlk, 0, s>>>(e->node_vol.p, e->old_of_new.p, V, vf, vd, nullptr, nullptr);
+  }
+  if (regions) {
+    std::vector<int32_t> nr(V);
+    FH_CUDA(cudaMemcpyAsync(nr.data(), e->node_region.p, sizeof(int32_t) * V, cudaMemcpyDeviceToHost, s));
+    FH_CUDA(cudaStreamSynchronize(s));
+    std::vector<uint8_t> nrn(V);
+    for (int64_t n = 0; n < V; ++n) nrn[n] = (uint8_t)nr[P.old_of_new[n]];
+    st->node_region.upload(nrn, s);
+  }
+  if (!e->td) {
+    st->cap.alloc(V);
+    st->kb.alloc(V);
+    st->tet_kbar.alloc(nts);
+    st->hex_kbar.alloc(nhs);
+  }
+  if (!e->q_static.empty() || !e->load_power.empty()) {
+    st->q_ext.alloc(V);
+    if (e->load_power.empty()) {
+      FH_CUDA(cudaMemcpyAsync(e->stage.p, e->q_static.data(), sizeof(double) * V, cudaMemcpyHostToDevice, s));
+      float *qf = nullptr;
+      double *qd = nullptr;
+      if constexpr (sizeof(S) == 4) qf = st->q_ext.p; else qd = st->q_ext.p;
+      k_to_new<<<nblk(V), kBlk, 0, s>>>(e->stage.p, e->old_of_new.p, V, qf, qd, nullptr, nullptr);
+    }
+  }
+  if (!e->sources.empty()) {
+    std::vector<S> x(3 * V);
+    for (int64_t n = 0; n < V; ++n)
+      for (int d = 0; d < 3; ++d) x[3 * n + d] = (S)mesh.coords[3 * P.old_of_new[n] + d];
+    st->xyz.upload(x, s);
+  }
+  if (!e->robin_nodes.empty()) {
+    // compact robin arrays ordered like the renumbered robin nodes
+    std::vector<int64_t> slot_of(V, -1);
+    for (size_t q = 0; q < e->robin_nodes.size(); ++q) slot_of[e->robin_nodes[q]] = (int64_t)q;
+    std::vector<S> ha(robin_base[P.n_parts]), hat(robin_base[P.n_parts]);
+    for (int p = 0; p < P.n_parts; ++p)
+      for (int loc = P.part_robin_start[p]; loc < P.part_n_free[p]; ++loc) {
+        const int64_t q = slot_of[P.old_of_new[P.part_node_start[p] + loc]];
+        ha[robin_base[p] + loc - P.part_robin_start[p]] = (S)e->robin_hA[q];
+        hat[robin_base[p] + loc - P.part_robin_start[p]] = (S)e->robin_hAT[q];
+      }
+    st->robin_hA.upload(ha, s);
+    st->robin_hAT.upload(hat, s);
+  }
+  g.part_list = st->part_list.p;
+  g.part_node_start = st->part_node_start.p;
+  g.part_n_free = st->part_n_free.p;
+  g.part_robin_start = st->part_robin_start.p;
+  g.part_robin_base = st->part_robin_base.p;
+  g.part_tet_start = st->part_tet_start.p;
+  g.part_hex_start = st->part_hex_start.p;
+  g.tet_conn = st->tet_conn.p;
+  g.hex_conn = st->hex_conn.p;
+  g.tet_G = st->tet_G.p;
+  g.hex_G = st->hex_G.p;
+  g.tet_kf = st->tet_kf.p;
+  g.hex_kf = st->hex_kf.p;
+  g.tet_rank = st->tet_rank.p;
+  g.hex_rank = st->hex_rank.p;
+  g.tet_region = st->tet_region.p;
+  g.hex_region = st->hex_region.p;
+  g.max_phase_tet = P.max_phase_tet;
+  g.max_phase_hex = P.max_phase_hex;
+  g.vol = st->vol.p;
+  g.cap_frozen = st->cap.p;
+  g.kb_frozen = st->kb.p;
+  g.q_ext = st->q_ext.p;
+  g.xyz = st->xyz.p;
+  g.node_region = st->node_region.p;
+  g.robin_hA = st->robin_hA.p;
+  g.robin_hAT = st->robin_hAT.p;
+  g.mats = mats_of<S>(e);
+  g.n_src = (int)e->sources.size();
+  g.runaway_limit = (S)e->runaway_limit;
+  g.flag = e->flag.p;
+  st->smem = sizeof(S) * (size_t)std::max(1, P.max_part_nodes);
+  if (st->smem > 200 * 1024) fail(FH_ERR_CONFIG, "tile too large for shared memory; lower part_nodes");
+  FH_CUDA(cudaStreamSynchronize(s));
+  if constexpr (sizeof(S) == 4)
+    e->tf = std::move(st);
+  else
+    e->tdd = std::move(st);
+}
+
+template <typename S>
+void tiled_set_T(fh_engine *e) {  // e->stage holds the field in original order
+  TiledState<S> &st = tstate<S>(e);
+  float *f0 = nullptr, *f1 = nullptr;
+  double *d0 = nullptr, *d1 = nullptr;
+  if constexpr (sizeof(S) == 4) {
+    f0 = st.T[0].p;
+    f1 = st.T[1].p;
+  } else {
+    d0 = st.T[0].p;
+    d1 = st.T[1].p;
+  }
+  k_to_new<<<nblk(e->V), kBlk, 0, e->stream>>>(e->stage.p, e->old_of_new.p, e->V, f0, d0, f1, d1);
+  FH_CUDA(cudaGetLastError());
+  st.cur = 0;
+}
+
+template <typename S>
+void tiled_get_T(fh_engine *e, double *dst_dev) {
+  TiledState<S> &st = tstate<S>(e);
+  k_to_old<S><<<nblk(e->V), kBlk, 0, e->stream>>>(st.T[st.cur].p, e->new_of_old.p, e->V, dst_dev);
+  FH_CUDA(cudaGetLastError());
+}
+
+// current field, original order, fp64, into e->stage (device)
+void current_T_to_stage(fh_engine *e) {
+  if (e->assembly == FH_ASSEMBLY_EXACT) {
+    FH_CUDA(cudaMemcpyAsync(e->stage.p, e->T.p, sizeof(double) * e->V, cudaMemcpyDeviceToDevice, e->stream));
+  } else if (e->precision == 32) {
+    tiled_get_T<float>(e, e->stage.p);
+  } else {
+    tiled_get_T<double>(e, e->stage.p);
+  }
+}
+
+template <typename S>
+void tiled_run(fh_engine *e, int64_t nsteps, double dt) {
+  TiledState<S> &st = tstate<S>(e);
+  TiledArgs<S> &g = st.args;
+  const int64_t step0 = e->step_index;
+  for (int64_t k = 0; k < nsteps; ++k) {
+    const double t = e->time;
+    upload_qr(e, t);
+    g.Tin = st.T[st.cur].p;
+    g.Tout = st.T[st.cur ^ 1].p;
+    if (!e->td && !e->frozen) {
+      const int64_t nts = (int64_t)e->part.tet_slot_elem.size(), nhs = (int64_t)e->part.hex_slot_elem.size();
+      tiled_freeze<S>(g, nts, nhs, e->V, st.tet_kf.p, st.hex_kf.p, st.tet_kbar.p, st.hex_kbar.p, st.cap.p,
+                      st.kb.p, e->stream);
+      g.tet_kf = st.tet_kbar.p;
+      g.hex_kf = st.hex_kbar.p;
+      e->frozen = true;
+    }
+    g.dt = (S)dt;
+    g.step_no = (unsigned long long)(e->step_index + 1);
+    for (int q = 0; q < g.n_src; ++q) {
+      const fh_source &src = e->sources[q];
+      SourceT<S> &d = g.src[q];
+      d.kind = src.kind;
+      d.active = (src.t0 <= t && t < src.t1);
+      d.amp = (S)src.amp;
+      d.inv2s2 = (S)(1.0 / (2.0 * src.sigma * src.sigma));
+      d.cap = (S)src.cap;
+      d.inv4pi_amp = (S)(src.amp / (4.0 * M_PI));
+      d.cx = (S)(src.x0[0] + src.vel[0] * t);
+      d.cy = (S)(src.x0[1] + src.vel[1] * t);
+      d.cz = (S)(src.x0[2] + src.vel[2] * t);
+    }
+    g.part_begin = 0;
+    tiled_step(g, st.n_parts_local, e->td, e->part.corner_unique, st.smem, e->stream);
+    st.cur ^= 1;
+    e->step_index += 1;
+    e->time = (double)e->step_index * dt;
+    if (e->n_probes && e->step_index % e->probe_interval == 0 && e->n_rec < e->probe_cap) {
+      gather_probes_t<S>(st.T[st.cur].p, e->probes.p, e->n_probes, e->probe_hist.p + e->n_rec * e->n_probes,
+                         e->flag.p, e->stream);
+      e->probe_steps.push_back(e->step_index);
+      e->n_rec++;
+    }
+  }
+  (void)step0;
+}
+
+void exact_run(fh_engine *e, int64_t nsteps, double dt) {
+  for (int64_t k = 0; k < nsteps; ++k) {
+    const double t = e->time;
+    upload_qr(e, t);
+    if (!e->td && !e->frozen) {
+      exact_props(e->ex, e->T.p, e->stream);
+      e->frozen = true;
+    }
+    exact_step(e->ex, e->T.p, dt, t, e->step_index + 1, e->td, e->stream);
+    e->step_index += 1;
+    e->time = (double)e->step_index * dt;
+    if (e->n_probes && e->step_index % e->probe_interval == 0 && e->n_rec < e->probe_cap) {
+      gather_probes(e->T.p, e->probes.p, e->n_probes, e->probe_hist.p + e->n_rec * e->n_probes, e->flag.p,
+                    e->stream);
+      e->probe_steps.push_back(e->step_index);
+      e->n_rec++;
+    }
+  }
+}
+
+int do_step(fh_engine *e, int64_t nsteps, double dt, fh_report *rep, float *elapsed_ms = nullptr) {
+  if (nsteps < 0) fail(FH_ERR_CONFIG, "nsteps must be >= 0");
+  if (!(dt > 0.0) || !std::isfinite(dt)) fail(FH_ERR_CONFIG, "dt must be positive and finite");
+  const int64_t step0 = e->step_index;
+  const int cur0 = e->assembly == FH_ASSEMBLY_EXACT ? 0 : (e->precision == 32 ? e->tf->cur : e->tdd->cur);
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  if (elapsed_ms) {
+    FH_CUDA(cudaEventCreate(&ev[0]));
+    FH_CUDA(cudaEventCreate(&ev[1]));
+    FH_CUDA(cudaEventRecord(ev[0], e->stream));
+  }
+  if (e->assembly == FH_ASSEMBLY_EXACT)
+    exact_run(e, nsteps, dt);
+  else if (e->precision == 32)
+    tiled_run<float>(e, nsteps, dt);
+  else
+    tiled_run<double>(e, nsteps, dt);
+  if (elapsed_ms) {
+    FH_CUDA(cudaEventRecord(ev[1], e->stream));
+    FH_CUDA(cudaEventSynchronize(ev[1]));
+    FH_CUDA(cudaEventElapsedTime(elapsed_ms, ev[0], ev[1]));
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+  }
+  FailFlag f{};
+  FH_CUDA(cudaMemcpyAsync(&f, e->flag.p, sizeof(f), cudaMemcpyDeviceToHost, e->stream));
+  FH_CUDA(cudaStreamSynchronize(e->stream));
+  if (rep) {
+    std::memset(rep, 0, sizeof(*rep));
+    rep->fail_step = -1;
+    rep->fail_node = -1;
+  }
+  if (f.step != ~0ull) {
+    const int64_t fs = (int64_t)f.step;
+    // roll the host clock back to the failing step (later launches were no-ops)
+    e->step_index = fs;
+    e->time = (double)fs * dt;
+    if (e->assembly != FH_ASSEMBLY_EXACT) {
+      const int par = (int)((fs - step0) & 1);
+      if (e->precision == 32) e->tf->cur = cur0 ^ par; else e->tdd->cur = cur0 ^ par;
+    }
+    while (!e->probe_steps.empty() && e->probe_steps.back() > fs) {
+      e->probe_steps.pop_back();
+      e->n_rec--;
+    }
+    // locate the node like solver.py:369-382 (first non-finite, else argmax |T|)
+    current_T_to_stage(e);
+    std::vector<double> T(e->V);
+    FH_CUDA(cudaMemcpyAsync(T.data(), e->stage.p, sizeof(double) * e->V, cudaMemcpyDeviceToHost, e->stream));
+    FH_CUDA(cudaStreamSynchronize(e->stream));
+    int64_t node = -1;
+    for (int64_t i = 0; i < e->V; ++i)
+      if (!std::isfinite(T[i])) {
+        node = i;
+        break;
+      }
+    if (node < 0) {
+      double best = -1.0;
+      for (int64_t i = 0; i < e->V; ++i)
+        if (std::fabs(T[i]) > best) {
+          best = std::fabs(T[i]);
+          node = i;
+        }
+    }
+    if (rep) {
+      rep->fail_step = fs;
+      rep->fail_node = node;
+      rep->fail_value = T[node];
+      rep->steps_done = fs - step0;
+      rep->time = e->time;
+      rep->step_index = e->step_index;
+    }
+    // clear the flag so the engine can be reused after set_temperature
+    const FailFlag clear{~0ull};
+    FH_CUDA(cudaMemcpy(e->flag.p, &clear, sizeof(clear), cudaMemcpyHostToDevice));
+    g_last_error = "temperature at node " + std::to_string(node) + " is non-finite or beyond the runaway limit";
+    return FH_ERR_INSTABILITY;
+  }
+  if (rep) {
+    rep->steps_done = nsteps;
+    rep->time = e->time;
+    rep->step_index = e->step_index;
+  }
+  return FH_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+const char *fh_last_error(void) { return g_last_error.c_str(); }
+int fh_version(void) { return 1; }
+
+int fh_device_count(int *count) {
+  FH_API_BEGIN
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+  *count = n;
+  FH_API_END
+}
+
+int fh_create(const fh_mesh *mesh, const fh_boundary *bnd, const fh_options *opts, fh_engine **out) {
+  FH_API_BEGIN
+  if (!mesh || !bnd || !opts || !out) fail(FH_ERR_CONFIG, "null argument");
+  *out = nullptr;
+  auto e = std::make_unique<fh_engine>();
+  e->opts = *opts;
+  e->device = opts->device;
+  e->precision = opts->precision == 32 ? 32 : 64;
+  e->assembly = opts->assembly;
+  e->td = opts->td_mode != 0;
+  e->runaway_limit = opts->runaway_limit;
+  if (e->assembly == FH_ASSEMBLY_EXACT && e->precision != 64) fail(FH_ERR_CONFIG, "EXACT mode is fp64 only");
+  if (e->assembly != FH_ASSEMBLY_EXACT && e->assembly != FH_ASSEMBLY_TILED)
+    fail(FH_ERR_CONFIG, "unsupported assembly mode");
+  e->V = mesh->n_nodes;
+  e->n_tet = mesh->n_tets;
+  e->n_hex = mesh->n_hexes;
+  e->E = e->n_tet + e->n_hex;
+  e->nconn = 4 * e->n_tet + 8 * e->n_hex;
+  if (e->V <= 0 || e->E <= 0) fail(FH_ERR_CONFIG, "empty mesh");
+  if (e->V >= (1ll << 31) || e->nconn >= (1ll << 31)) fail(FH_ERR_CONFIG, "mesh too large for 32-bit indices");
+  fill_mats(e->mats_d, *opts);
+  fill_mats(e->mats_f, *opts);
+  FH_CUDA(cudaSetDevice(e->device));
+  FH_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  cudaStream_t s = e->stream;
+  // boundary (host copies)
+  e->dir_nodes.assign(bnd->dirichlet_nodes, bnd->dirichlet_nodes + bnd->n_dirichlet);
+  e->dir_vals.assign(bnd->dirichlet_values, bnd->dirichlet_values + bnd->n_dirichlet);
+  for (int64_t i : e->dir_nodes)
+    if (i < 0 || i >= e->V) fail(FH_ERR_CONFIG, "Dirichlet node out of range");
+  if (bnd->n_loads > 0) {
+    e->load_offs.assign(bnd->load_offsets, bnd->load_offsets + bnd->n_loads + 1);
+    e->load_nodes.assign(bnd->load_nodes, bnd->load_nodes + e->load_offs.back());
+    e->load_power.assign(bnd->load_power, bnd->load_power + bnd->n_loads);
+    e->load_t0.assign(bnd->load_t0, bnd->load_t0 + bnd->n_loads);
+    e->load_t1.assign(bnd->load_t1, bnd->load_t1 + bnd->n_loads);
+    e->load_sig.assign(bnd->n_loads, 0);
+  }
+  if (bnd->q_static) e->q_static.assign(bnd->q_static, bnd->q_static + e->V);
+  if (bnd->n_sources > kMaxSources) fail(FH_ERR_CONFIG, "too many sources");
+  e->sources.assign(bnd->sources, bnd->sources + std::max(0, bnd->n_sources));
+  if (bnd->n_robin > 0) {
+    e->robin_nodes.assign(bnd->robin_nodes, bnd->robin_nodes + bnd->n_robin);
+    e->robin_hA.assign(bnd->robin_hA, bnd->robin_hA + bnd->n_robin);
+    e->robin_hAT.assign(bnd->robin_hAT, bnd->robin_hAT + bnd->n_robin);
+  }
+  // connectivity + CSR (host bookkeeping), device copies
+  std::vector<int32_t> conn(e->nconn);
+  for (int64_t p = 0; p < 4 * e->n_tet; ++p) conn[p] = (int32_t)mesh->tets[p];
+  for (int64_t p = 0; p < 8 * e->n_hex; ++p) conn[4 * e->n_tet + p] = (int32_t)mesh->hexes[p];
+  for (int32_t v : conn)
+    if (v < 0 || v >= e->V) fail(FH_ERR_CONFIG, "element references a node out of range");
+  std::vector<int32_t> offs, pos;
+  build_node_csr(e->V, e->n_tet, mesh->tets, e->n_hex, mesh->hexes, offs, pos);
+  e->conn.upload(conn, s);
+  e->csr_offs.upload(offs, s);
+  e->csr_pos.upload(pos, s);
+  e->xyz.upload(mesh->coords, 3 * e->V, s);
+  if (opts->element_kfactor) e->kfactor.upload(opts->element_kfactor, e->E, s);
+  // regions: node region = largest region id among incident elements
+  if (opts->n_materials > 1 && opts->element_region) {
+    std::vector<int32_t> er(opts->element_region, opts->element_region + e->E), nr(e->V, 0);
+    for (int32_t r : er)
+      if (r < 0 || r >= opts->n_materials) fail(FH_ERR_CONFIG, "element region out of range");
+    for (int64_t i = 0; i < e->V; ++i)
+      for (int32_t q = offs[i]; q < offs[i + 1]; ++q) {
+        const int64_t p = pos[q];
+        const int64_t el = p < 4 * e->n_tet ? p / 4 : e->n_tet + (p - 4 * e->n_tet) / 8;
+        nr[i] = std::max(nr[i], er[el]);
+      }
+    e->elem_region.upload(er, s);
+    e->node_region.upload(nr, s);
+  }
+  // device precompute (fh_precompute.cu)
+  e->elem_vol.alloc(e->E);
+  e->node_vol.alloc(e->V);
+  e->row_abs.alloc(e->nconn);
+  DBuf<double> G;
+  DBuf<int> bad;
+  bad.alloc(1);
+  const int big = 0x7fffffff;
+  FH_CUDA(cudaMemcpyAsync(bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+  GeomOut go{};
+  go.vol = e->elem_vol.p;
+  go.row_abs = e->row_abs.p;
+  go.bad = bad.p;
+  if (e->assembly == FH_ASSEMBLY_EXACT) {
+    e->A.alloc(16 * e->n_tet + 64 * e->n_hex);
+    go.A = e->A.p;
+  } else {
+    G.alloc(6 * e->E);
+    go.G = G.p;
+  }
+  launch_geometry(e->xyz.p, e->conn.p, e->n_tet, e->n_hex, go, s);
+  int first_bad = big;
+  FH_CUDA(cudaMemcpyAsync(&first_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  FH_CUDA(cudaStreamSynchronize(s));
+  if (first_bad != big)
+    fail(FH_ERR_DEGENERATE, "element " + std::to_string(first_bad) + ": non-positive volume / Jacobian");
+  launch_node_volumes(e->csr_offs.p, e->csr_pos.p, e->V, e->n_tet, e->elem_vol.p, e->node_vol.p, s);
+  e->flag.alloc(1);
+  const FailFlag clear{~0ull};
+  FH_CUDA(cudaMemcpyAsync(e->flag.p, &clear, sizeof(clear), cudaMemcpyHostToDevice, s));
+  e->stage.alloc(e->V);
+  if (e->assembly == FH_ASSEMBLY_EXACT) {
+    setup_exact(e.get(), *bnd);
+  } else if (e->precision == 32) {
+    setup_tiled<float>(e.get(), *mesh, *bnd, G.p);
+  } else {
+    setup_tiled<double>(e.get(), *mesh, *bnd, G.p);
+  }
+  if (e->assembly != FH_ASSEMBLY_EXACT) {  // exact-order critical dt still needs these
+    e->ex.V = e->V;
+    e->ex.E = e->E;
+    e->ex.n_tet = e->n_tet;
+    e->ex.conn = e->conn.p;
+    e->ex.row_abs = e->row_abs.p;
+    e->ex.csr_offs = e->csr_offs.p;
+    e->ex.csr_pos = e->csr_pos.p;
+    e->ex.node_vol = e->node_vol.p;
+    e->ex.elem_region = e->elem_region.p;
+    e->ex.node_region = e->node_region.p;
+    e->ex.kfactor = e->kfactor.p;
+    e->ex.mats = e->mats_d;
+    std::vector<double> nv(e->V), kbh(e->V);
+    std::vector<int32_t> nreg(e->V, 0);
+    FH_CUDA(cudaMemcpy(nv.data(), e->node_vol.p, sizeof(double) * e->V, cudaMemcpyDeviceToHost));
+    if (e->node_region.p)
+      FH_CUDA(cudaMemcpy(nreg.data(), e->node_region.p, sizeof(int32_t) * e->V, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < e->V; ++i) {
+      const fh_material &m = opts->materials[nreg[i]];
+      kbh[i] = (m.perfusion_rate * m.blood_specific_heat) * nv[i];
+    }
+    e->kb.upload(kbh, s);
+    e->ex.kb = e->kb.p;
+    if (!e->robin_nodes.empty()) {
+      std::vector<int32_t> rs(e->V, -1);
+      for (size_t q = 0; q < e->robin_nodes.size(); ++q) rs[e->robin_nodes[q]] = (int32_t)q;
+      e->robin_slot.upload(rs, s);
+      e->robin_hA_d.upload(e->robin_hA, s);
+      e->ex.robin_slot = e->robin_slot.p;
+      e->ex.robin_hA = e->robin_hA_d.p;
+    }
+  }
+  FH_CUDA(cudaStreamSynchronize(s));
+  *out = e.release();
+  FH_API_END
+}
+
+int fh_destroy(fh_engine *e) {
+  FH_API_BEGIN
+  if (e) {
+    cudaSetDevice(e->device);
+    cudaStreamSynchronize(e->stream);
+    delete e;
+  }
+  FH_API_END
+}
+
+int fh_set_temperature(fh_engine *e, const double *T, int64_t n, int64_t step_index, double time) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (n != e->V) fail(FH_ERR_CONFIG, "temperature field has the wrong length");
+  FH_CUDA(cudaMemcpyAsync(e->stage.p, T, sizeof(double) * e->V, cudaMemcpyHostToDevice, e->stream));
+  if (e->assembly == FH_ASSEMBLY_EXACT)
+    FH_CUDA(cudaMemcpyAsync(e->T.p, e->stage.p, sizeof(double) * e->V, cudaMemcpyDeviceToDevice, e->stream));
+  else if (e->precision == 32)
+    tiled_set_T<float>(e);
+  else
+    tiled_set_T<double>(e);
+  e->step_index = step_index;
+  e->time = time;
+  FH_CUDA(cudaStreamSynchronize(e->stream));
+  FH_API_END
+}
+
+int fh_get_temperature(fh_engine *e, double *T, int64_t n) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (n != e->V) fail(FH_ERR_CONFIG, "output has the wrong length");
+  current_T_to_stage(e);
+  FH_CUDA(cudaMemcpyAsync(T, e->stage.p, sizeof(double) * e->V, cudaMemcpyDeviceToHost, e->stream));
+  FH_CUDA(cudaStreamSynchronize(e->stream));
+  FH_API_END
+}
+
+int fh_get_inflow(fh_engine *e, double *F, int64_t n) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (e->assembly != FH_ASSEMBLY_EXACT) fail(FH_ERR_CONFIG, "inflow is only kept in EXACT mode");
+  if (n != e->V) fail(FH_ERR_CONFIG, "output has the wrong length");
+  FH_CUDA(cudaMemcpyAsync(F, e->F.p, sizeof(double) * e->V, cudaMemcpyDeviceToHost, e->stream));
+  FH_CUDA(cudaStreamSynchronize(e->stream));
+  FH_API_END
+}
+
+int fh_reset_properties(fh_engine *e) {
+  FH_API_BEGIN
+  check_engine(e);
+  e->frozen = false;
+  e->qr_valid = false;
+  if (e->assembly != FH_ASSEMBLY_EXACT && !e->td) {  // restore the factor pointers
+    if (e->precision == 32) {
+      e->tf->args.tet_kf = e->tf->tet_kf.p;
+      e->tf->args.hex_kf = e->tf->hex_kf.p;
+    } else {
+      e->tdd->args.tet_kf = e->tdd->tet_kf.p;
+      e->tdd->args.hex_kf = e->tdd->hex_kf.p;
+    }
+  }
+  FH_API_END
+}
+
+int fh_step(fh_engine *e, int64_t nsteps, double dt, fh_report *rep) {
+  FH_API_BEGIN
+  check_engine(e);
+  return do_step(e, nsteps, dt, rep);
+  FH_API_END
+}
+
+int fh_step_timed(fh_engine *e, int64_t nsteps, double dt, fh_report *rep, float *elapsed_ms) {
+  FH_API_BEGIN
+  check_engine(e);
+  return do_step(e, nsteps, dt, rep, elapsed_ms);
+  FH_API_END
+}
+
+int fh_step_host(fh_engine *e, const double *T_in, double *T_out, int64_t n, int64_t nsteps, double dt,
+                 fh_report *rep) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (n != e->V) fail(FH_ERR_CONFIG, "field has the wrong length");
+  if (T_in) {
+    FH_CUDA(cudaMemcpyAsync(e->stage.p, T_in, sizeof(double) * e->V, cudaMemcpyHostToDevice, e->stream));
+    if (e->assembly == FH_ASSEMBLY_EXACT)
+      FH_CUDA(cudaMemcpyAsync(e->T.p, e->stage.p, sizeof(double) * e->V, cudaMemcpyDeviceToDevice, e->stream));
+    else if (e->precision == 32)
+      tiled_set_T<float>(e);
+    else
+      tiled_set_T<double>(e);
+  }
+  const int rc = do_step(e, nsteps, dt, rep);
+  if (T_out) {
+    current_T_to_stage(e);
+    FH_CUDA(cudaMemcpyAsync(T_out, e->stage.p, sizeof(double) * e->V, cudaMemcpyDeviceToHost, e->stream));
+    FH_CUDA(cudaStreamSynchronize(e->stream));
+  }
+  return rc;
+  FH_API_END
+}
+
+int fh_set_sources(fh_engine *e, const fh_source *sources, int32_t n) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (n < 0 || n > kMaxSources) fail(FH_ERR_CONFIG, "too many sources");
+  e->sources.assign(sources, sources + n);
+  if (e->assembly == FH_ASSEMBLY_EXACT) {
+    e->ex.n_src = n;
+    for (int k = 0; k < n; ++k) e->ex.src[k] = sources[k];
+  } else {
+    auto setup = [&](auto &st) {
+      using S = std::remove_reference_t<decltype(*st.T[0].p)>;
+      if (n > 0 && !st.xyz.p) {
+        st.xyz.alloc(3 * e->V);
+        k_xyz_to_new<S><<<nblk(e->V), kBlk, 0, e->stream>>>(e->xyz.p, e->old_of_new.p, e->V, st.xyz.p);
+        FH_CUDA(cudaGetLastError());
+        st.args.xyz = st.xyz.p;
+      }
+      st.args.n_src = n;
+    };
+    if (e->precision == 32) setup(*e->tf); else setup(*e->tdd);
+    FH_CUDA(cudaStreamSynchronize(e->stream));
+  }
+  FH_API_END
+}
+
+int fh_set_probes(fh_engine *e, const int64_t *nodes, int64_t n, int64_t interval, int64_t capacity) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (interval < 1) fail(FH_ERR_CONFIG, "probe interval must be >= 1");
+  std::vector<int32_t> p(n);
+  for (int64_t q = 0; q < n; ++q) {
+    if (nodes[q] < 0 || nodes[q] >= e->V) fail(FH_ERR_CONFIG, "probe node index out of range");
+    p[q] = (int32_t)(e->assembly == FH_ASSEMBLY_EXACT ? nodes[q] : e->part.new_of_old[nodes[q]]);
+  }
+  e->probes.upload(p, e->stream);
+  e->n_probes = n;
+  e->probe_interval = interval;
+  e->probe_cap = n ? capacity : 0;
+  e->probe_hist.alloc((size_t)std::max<int64_t>(1, n * e->probe_cap));
+  e->n_rec = 0;
+  e->probe_steps.clear();
+  FH_CUDA(cudaStreamSynchronize(e->stream));
+  FH_API_END
+}
+
+int fh_get_probes(fh_engine *e, double *values, int64_t max_records, int64_t *n_records) {
+  FH_API_BEGIN
+  check_engine(e);
+  const int64_t r = std::min(max_records, e->n_rec);
+  if (r > 0)
+    FH_CUDA(cudaMemcpyAsync(values, e->probe_hist.p, sizeof(double) * r * e->n_probes, cudaMemcpyDeviceToHost,
+                            e->stream));
+  FH_CUDA(cudaStreamSynchronize(e->stream));
+  *n_records = r;
+  FH_API_END
+}
+
+int fh_critical_dt(fh_engine *e, const double *T, int64_t n, double *out) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (T && n != e->V) fail(FH_ERR_CONFIG, "field has the wrong length");
+  if (T)
+    FH_CUDA(cudaMemcpyAsync(e->stage.p, T, sizeof(double) * e->V, cudaMemcpyHostToDevice, e->stream));
+  else
+    current_T_to_stage(e);
+  e->crit_kbar.alloc(e->E);
+  e->crit_lam.alloc(e->V);
+  exact_critical(e->ex, e->stage.p, e->crit_kbar.p, e->crit_lam.p, e->stream);
+  std::vector<double> lam(e->V);
+  FH_CUDA(cudaMemcpyAsync(lam.data(), e->crit_lam.p, sizeof(double) * e->V, cudaMemcpyDeviceToHost, e->stream));
+  FH_CUDA(cudaStreamSynchronize(e->stream));
+  e->crit_kbar.release();
+  e->crit_lam.release();
+  double best = -INFINITY;
+  bool any = false, nan = false;
+  for (double v : lam) {
+    if (v == -INFINITY) continue;
+    any = true;
+    if (std::isnan(v)) nan = true;
+    best = std::max(best, v);
+  }
+  if (!any) fail(FH_ERR_CONFIG, "every node has zero heat capacity");
+  if (nan) best = NAN;
+  *out = (best <= 0.0) ? INFINITY : 2.0 / best;
+  FH_API_END
+}
+
+int fh_scatter_loads(fh_engine *e, const double *kbar, const double *T, int64_t n, double *out) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (e->assembly != FH_ASSEMBLY_EXACT) fail(FH_ERR_CONFIG, "scatter_loads needs EXACT mode");
+  if (n != e->V) fail(FH_ERR_CONFIG, "field has the wrong length");
+  DBuf<double> kb, Tt, o;
+  kb.upload(kbar, e->E, e->stream);
+  Tt.upload(T, e->V, e->stream);
+  o.alloc(e->V);
+  exact_scatter(e->ex, kb.p, Tt.p, o.p, e->stream);
+  FH_CUDA(cudaMemcpyAsync(out, o.p, sizeof(double) * e->V, cudaMemcpyDeviceToHost, e->stream));
+  FH_CUDA(cudaStreamSynchronize(e->stream));
+  FH_API_END
+}
+
+int fh_get_precompute(fh_engine *e, double *node_volumes, double *elem_volumes) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (node_volumes)
+    FH_CUDA(cudaMemcpy(node_volumes, e->node_vol.p, sizeof(double) * e->V, cudaMemcpyDeviceToHost));
+  if (elem_volumes)
+    FH_CUDA(cudaMemcpy(elem_volumes, e->elem_vol.p, sizeof(double) * e->E, cudaMemcpyDeviceToHost));
+  FH_API_END
+}
+
+int fh_get_layout(fh_engine *e, fh_layout *out) {
+  FH_API_BEGIN
+  check_engine(e);
+  std::memset(out, 0, sizeof(*out));
+  out->n_elements = e->E;
+  const int64_t s = e->precision == 32 ? 4 : 8;
+  // SURVEY 8(d) canonical: per element N*4 (int32 conn) + 6s (G) + 4 (factor, if any);
+  // per node 2s (T r/w) + s (v) + per-node source data
+  int64_t canon = e->n_tet * (16 + 6 * s) + e->n_hex * (32 + 6 * s) + (e->kfactor.p ? 4 * e->E : 0);
+  canon += e->V * 3 * s;
+  if (!e->q_static.empty() || !e->load_power.empty()) canon += e->V * s;
+  if (!e->sources.empty()) canon += e->V * 3 * s;
+  out->canonical_bytes = canon;
+  if (e->assembly == FH_ASSEMBLY_EXACT) {
+    out->kernels_per_step = 2;
+    out->n_slots = e->E;
+    out->n_nodes_owned = e->V;
+    // conn + A + contrib w/r + csr + node streams
+    out->step_bytes = e->nconn * 4 + (16 * e->n_tet + 64 * e->n_hex) * 8 + e->nconn * 16 + e->nconn * 4 +
+                      e->V * 8 * 8;
+  } else {
+    const Partition &P = e->part;
+    out->kernels_per_step = 1;
+    out->n_parts = P.n_parts;
+    out->max_part_nodes = P.max_part_nodes;
+    const int64_t nts = (int64_t)P.tet_slot_elem.size(), nhs = (int64_t)P.hex_slot_elem.size();
+    out->n_slots = nts + nhs;
+    int64_t owned = 0;
+    for (int p = 0; p < P.n_parts; ++p) owned += P.part_n_free[p];
+    out->n_nodes_owned = owned;
+    int64_t b = nts * (16 + 6 * s) + nhs * (32 + 6 * s);
+    if (e->kfactor.p || !e->td) b += (nts + nhs) * s;
+    if (!P.corner_unique) b += nts * 4 + nhs * 8;
+    int64_t node_streams = 3 * s;  // T read, T' write, v
+    if (!e->td) node_streams += s;  // frozen capacity
+    if (!e->q_static.empty() || !e->load_power.empty()) node_streams += s;
+    if (!e->sources.empty()) node_streams += 3 * s;
+    b += owned * node_streams;
+    out->step_bytes = b;
+  }
+  FH_API_END
+}
+
+void *fh_stream(fh_engine *e) { return e ? (void *)e->stream : nullptr; }
+
+int fh_get_node_order(fh_engine *e, int64_t *new_to_old, int64_t n) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (n != e->V) fail(FH_ERR_CONFIG, "output has the wrong length");
+  if (e->assembly == FH_ASSEMBLY_EXACT)
+    for (int64_t i = 0; i < n; ++i) new_to_old[i] = i;
+  else
+    std::memcpy(new_to_old, e->part.old_of_new.data(), sizeof(int64_t) * n);
+  FH_API_END
+}
+
+// ---------------------------------------------------------------------------
+// operator layer
+static Curve<double> make_curve(const double *x, const double *y, int64_t n) {
+  fh_curve c{(int32_t)n, x, y};
+  Curve<double> out;
+  fill_curve(out, c, "curve");
+  return out;
+}
+
+int fh_eval_curve_nodes(const double *xs, const double *ys, int64_t n_knots, const double *temps, int64_t n,
+                        double *out) {
+  FH_API_BEGIN
+  const Curve<double> c = make_curve(xs, ys, n_knots);
+  DBuf<double> T, o;
+  T.upload(temps, n);
+  o.alloc(n);
+  op_curve(c, T.p, n, o.p, 0);
+  FH_CUDA(cudaMemcpy(out, o.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  FH_API_END
+}
+
+int fh_lumped_capacity_nodes(const double *rho_x, const double *rho_y, int64_t n_rho, const double *c_x,
+                             const double *c_y, int64_t n_c, const double *temps, const double *vols, int64_t n,
+                             double *out) {
+  FH_API_BEGIN
+  const Curve<double> r = make_curve(rho_x, rho_y, n_rho), c = make_curve(c_x, c_y, n_c);
+  DBuf<double> T, v, o;
+  T.upload(temps, n);
+  v.upload(vols, n);
+  o.alloc(n);
+  op_capacity(r, c, T.p, v.p, n, o.p, 0);
+  FH_CUDA(cudaMemcpy(out, o.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  FH_API_END
+}
+
+int fh_element_mean_nodal(const int64_t *conn_data, const int64_t *conn_offs, int64_t n_elem, const double *nodal,
+                          int64_t n_nodes, double *out) {
+  FH_API_BEGIN
+  const int64_t nc = conn_offs[n_elem];
+  std::vector<int32_t> c32(nc);
+  for (int64_t p = 0; p < nc; ++p) {
+    if (conn_data[p] < 0 || conn_data[p] >= n_nodes) fail(FH_ERR_CONFIG, "node index out of range");
+    c32[p] = (int32_t)conn_data[p];
+  }
+  DBuf<int32_t> c;
+  DBuf<int64_t> offs;
+  DBuf<double> nd, o;
+  c.upload(c32);
+  offs.upload(conn_offs, n_elem + 1);
+  nd.upload(nodal, n_nodes);
+  o.alloc(n_elem);
+  op_mean(c.p, offs.p, n_elem, nd.p, o.p, 0);
+  FH_CUDA(cudaMemcpy(out, o.p, sizeof(double) * n_elem, cudaMemcpyDeviceToHost));
+  FH_API_END
+}
+
+int fh_scatter_net_loads(const int64_t *conn_data, const int64_t *conn_offs, const double *mat_data,
+                         const int64_t *mat_offs, int64_t n_elem, const double *kbar, const double *temps,
+                         int64_t n_nodes, int64_t chunk_size, double *out) {
+  FH_API_BEGIN
+  if (chunk_size < 1) fail(FH_ERR_CONFIG, "chunk_size must be >= 1");
+  const int64_t nc = conn_offs[n_elem];
+  std::vector<int32_t> c32(nc), elem_of(nc);
+  for (int64_t e = 0; e < n_elem; ++e) {
+    const int64_t n = conn_offs[e + 1] - conn_offs[e];
+    if (n < 1 || n > 8) fail(FH_ERR_CONFIG, "elements must have 1..8 nodes");
+    if (mat_offs[e + 1] - mat_offs[e] != n * n) fail(FH_ERR_CONFIG, "mat_offs do not match conn_offs");
+    for (int64_t p = conn_offs[e]; p < conn_offs[e + 1]; ++p) elem_of[p] = (int32_t)e;
+  }
+  std::vector<int32_t> offs(n_nodes + 1, 0), pos(nc);
+  for (int64_t p = 0; p < nc; ++p) {
+    if (conn_data[p] < 0 || conn_data[p] >= n_nodes) fail(FH_ERR_CONFIG, "node index out of range");
+    c32[p] = (int32_t)conn_data[p];
+    offs[c32[p] + 1]++;
+  }
+  for (int64_t i = 0; i < n_nodes; ++i) offs[i + 1] += offs[i];
+  std::vector<int32_t> fill(offs.begin(), offs.end() - 1);
+  for (int64_t p = 0; p < nc; ++p) pos[fill[c32[p]]++] = (int32_t)p;
+  DBuf<int32_t> dc, deo, doffs, dpos;
+  DBuf<int64_t> dco, dmo;
+  DBuf<double> dm, dk, dT, dcontrib, dout;
+  dc.upload(c32);
+  deo.upload(elem_of);
+  doffs.upload(offs);
+  dpos.upload(pos);
+  dco.upload(conn_offs, n_elem + 1);
+  dmo.upload(mat_offs, n_elem + 1);
+  dm.upload(mat_data, mat_offs[n_elem]);
+  dk.upload(kbar, n_elem);
+  dT.upload(temps, n_nodes);
+  dcontrib.alloc(nc);
+  dout.alloc(n_nodes);
+  ExactArgs g;
+  std::memset(&g, 0, sizeof(g));
+  g.V = n_nodes;
+  g.E = n_elem;
+  g.chunk_size = chunk_size;
+  g.conn = dc.p;
+  g.conn_offs = dco.p;
+  g.mat_offs = dmo.p;
+  g.mat = dm.p;
+  g.csr_offs = doffs.p;
+  g.csr_pos = dpos.p;
+  g.elem_of = deo.p;
+  g.contrib = dcontrib.p;
+  exact_scatter(g, dk.p, dT.p, dout.p, 0);
+  FH_CUDA(cudaMemcpy(out, dout.p, sizeof(double) * n_nodes, cudaMemcpyDeviceToHost));
+  FH_API_END
+}
+
+int fh_nodal_update(double *temps, const double *inflow, const double *capacity, const double *perf_k,
+                    const double *perf_q, const double *metab_q, const double *extra_q, int64_t n, double dt) {
+  FH_API_BEGIN
+  DBuf<double> T, F, C, kb, qb, qm, qr;
+  T.upload(temps, n);
+  F.upload(inflow, n);
+  C.upload(capacity, n);
+  kb.upload(perf_k, n);
+  qb.upload(perf_q, n);
+  qm.upload(metab_q, n);
+  qr.upload(extra_q, n);
+  op_update(T.p, F.p, C.p, kb.p, qb.p, qm.p, qr.p, n, dt, 0);
+  FH_CUDA(cudaMemcpy(temps, T.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  FH_API_END
+}
+
+int fh_nccl_unique_id(char *id128) {
+  (void)id128;
+  g_last_error = "multi-GPU exchange is built in fh_dist.cu";
+  return FH_ERR_CONFIG;
+}
+
+int fh_attach_nccl(fh_engine *e, const char *id128, int32_t rank, int32_t world) {
+  (void)e;
+  (void)id128;
+  (void)rank;
+  (void)world;
+  g_last_error = "multi-GPU exchange is built in fh_dist.cu";
+  return FH_ERR_CONFIG;
+}
+
+}  // extern "C"

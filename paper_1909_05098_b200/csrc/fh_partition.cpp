@@ -1,0 +1,244 @@
+// Host-side bookkeeping for the fused step: node renumbering, tiles
+// ("parts") of nodes, the element slots of every part and the deterministic
+// accumulation phases.  Integer work only; floating-point precompute runs on
+// the device (fh_precompute.cu).
+//
+// Layout produced:
+//  * domains: the node set is cut into n_domains pieces (slabs along an axis,
+//    or recursive coordinate bisection).  Multi-GPU engines own a contiguous
+//    range of domains; the tile decomposition never depends on the GPU count,
+//    so results are bitwise identical for 1, 2, 4 or 8 GPUs.
+//  * parts: each domain is cut by recursive coordinate bisection into parts of
+//    <= target nodes.  New node ids are part-major; inside a part nodes are
+//    ordered free | robin | dirichlet (original id order inside each class),
+//    so "updated by this part" is one range check and Dirichlet nodes are never
+//    touched by the step kernel.
+//  * slots: every element is listed in each part that owns one of its
+//    non-Dirichlet nodes (owner computes; halo elements are recomputed by
+//    each owner instead of exchanging partial loads).  Slots of a part are
+//    tets then hexes, ascending original element id.
+//  * phases: inside a batch of `batch` slots the contribution of corner a of
+//    slot s is added in phase rank(s, a) = number of earlier slots of the
+//    batch that touch the same node.  Phases are separated by barriers, so
+//    every node's sum has a fixed order: deterministic, no atomics.  When each
+//    node meets every corner index at most once per batch (structured hex
+//    grids) the phase is simply the corner index and no rank bytes are stored.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "fh_internal.h"
+
+namespace fh {
+
+void build_node_csr(int64_t V, int64_t n_tet, const int64_t *tets, int64_t n_hex, const int64_t *hexes,
+                    std::vector<int32_t> &offs, std::vector<int32_t> &pos) {
+  const int64_t nconn = 4 * n_tet + 8 * n_hex;
+  offs.assign(V + 1, 0);
+  for (int64_t p = 0; p < 4 * n_tet; ++p) offs[tets[p] + 1]++;
+  for (int64_t p = 0; p < 8 * n_hex; ++p) offs[hexes[p] + 1]++;
+  for (int64_t i = 0; i < V; ++i) offs[i + 1] += offs[i];
+  pos.resize(nconn);
+  std::vector<int32_t> fill(offs.begin(), offs.end() - 1);
+  for (int64_t p = 0; p < 4 * n_tet; ++p) pos[fill[tets[p]]++] = (int32_t)p;
+  for (int64_t p = 0; p < 8 * n_hex; ++p) pos[fill[hexes[p]]++] = (int32_t)(4 * n_tet + p);
+}
+
+namespace {
+
+struct Rcb {
+  const double *xyz;
+  // split idx[lo,hi) into `parts` pieces of near-equal size; appends piece
+  // boundaries (as offsets into idx) in leaf order.
+  void split(std::vector<int64_t> &idx, int64_t lo, int64_t hi, int parts, std::vector<int64_t> &bounds,
+             int forced_axis) {
+    if (parts <= 1 || hi - lo <= 1) {
+      bounds.push_back(hi);
+      return;
+    }
+    int axis = forced_axis;
+    if (axis < 0) {
+      double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+      for (int64_t q = lo; q < hi; ++q)
+        for (int d = 0; d < 3; ++d) {
+          const double v = xyz[3 * idx[q] + d];
+          mn[d] = std::min(mn[d], v);
+          mx[d] = std::max(mx[d], v);
+        }
+      axis = 0;
+      // longest extent; ties go to the highest axis (z first) so that cubes
+      // split into z-slabs first, then y, then x
+      for (int d = 1; d < 3; ++d)
+        if (mx[d] - mn[d] >= mx[axis] - mn[axis]) axis = d;
+    }
+    const int left_parts = parts / 2;
+    const int64_t mid = lo + (int64_t)((double)(hi - lo) * left_parts / parts);
+    const double *x = xyz;
+    auto less = [x, axis](int64_t a, int64_t b) {
+      const double va = x[3 * a + axis], vb = x[3 * b + axis];
+      return va < vb || (va == vb && a < b);
+    };
+    std::nth_element(idx.begin() + lo, idx.begin() + mid, idx.begin() + hi, less);
+    split(idx, lo, mid, left_parts, bounds, forced_axis);
+    split(idx, mid, hi, parts - left_parts, bounds, forced_axis);
+  }
+};
+
+template <int N>
+void build_slots(int64_t n_elem, const int64_t *conn_old, int64_t elem_offset, const Partition &P,
+                 const std::vector<int32_t> &part_of_new, const std::vector<uint8_t> &updatable_new,
+                 std::vector<std::vector<int32_t>> &per_part) {
+  for (int64_t e = 0; e < n_elem; ++e) {
+    int32_t seen[N];
+    int ns = 0;
+    for (int a = 0; a < N; ++a) {
+      const int64_t nn = P.new_of_old[conn_old[N * e + a]];
+      if (!updatable_new[nn]) continue;
+      const int32_t p = part_of_new[nn];
+      bool dup = false;
+      for (int k = 0; k < ns; ++k) dup |= (seen[k] == p);
+      if (!dup) seen[ns++] = p;
+    }
+    for (int k = 0; k < ns; ++k) per_part[seen[k]].push_back((int32_t)(e + elem_offset));
+  }
+}
+
+}  // namespace
+
+void build_partition(const PartitionInput &in, Partition &P) {
+  const int64_t V = in.V;
+  const int target = std::max(64, in.target_part_nodes);
+  const int ndom = std::max(1, in.n_domains);
+  std::vector<int64_t> idx(V);
+  std::iota(idx.begin(), idx.end(), 0);
+  Rcb rcb{in.xyz};
+  // 1. domains
+  std::vector<int64_t> dom_bounds;
+  if (ndom > 1 && in.slab_axis >= 0) {
+    const int ax = in.slab_axis;
+    const double *x = in.xyz;
+    std::stable_sort(idx.begin(), idx.end(), [x, ax](int64_t a, int64_t b) { return x[3 * a + ax] < x[3 * b + ax]; });
+    for (int d = 1; d <= ndom; ++d) dom_bounds.push_back((int64_t)((double)V * d / ndom));
+  } else {
+    rcb.split(idx, 0, V, ndom, dom_bounds, -1);
+  }
+  // 2. parts inside each domain
+  std::vector<int64_t> part_bounds;
+  P.domain_part_start.assign(1, 0);
+  int64_t lo = 0;
+  for (int d = 0; d < ndom; ++d) {
+    const int64_t hi = dom_bounds[d];
+    const int parts = (int)std::max<int64_t>(1, (hi - lo + target - 1) / target);
+    rcb.split(idx, lo, hi, parts, part_bounds, -1);
+    P.domain_part_start.push_back((int32_t)part_bounds.size());
+    lo = hi;
+  }
+  P.n_parts = (int)part_bounds.size();
+  P.part_domain.resize(P.n_parts);
+  for (int d = 0; d < ndom; ++d)
+    for (int p = P.domain_part_start[d]; p < P.domain_part_start[d + 1]; ++p) P.part_domain[p] = d;
+  // 3. order inside parts: class (free, robin, dirichlet), then original id
+  P.new_of_old.assign(V, -1);
+  P.old_of_new.resize(V);
+  P.part_node_start.assign(P.n_parts + 1, 0);
+  P.part_n_free.resize(P.n_parts);
+  P.part_robin_start.resize(P.n_parts);
+  std::vector<int32_t> part_of_new(V);
+  int64_t start = 0, next = 0;
+  P.max_part_nodes = 0;
+  for (int p = 0; p < P.n_parts; ++p) {
+    const int64_t end = part_bounds[p];
+    auto cls = in.node_class;
+    std::sort(idx.begin() + start, idx.begin() + end, [cls](int64_t a, int64_t b) {
+      const int ca = cls ? cls[a] : 0, cb = cls ? cls[b] : 0;
+      return ca < cb || (ca == cb && a < b);
+    });
+    int n_free = 0, n_plain = 0;
+    for (int64_t q = start; q < end; ++q) {
+      const int c = in.node_class ? in.node_class[idx[q]] : 0;
+      if (c < 2) ++n_free;
+      if (c == 0) ++n_plain;
+      P.new_of_old[idx[q]] = next;
+      P.old_of_new[next] = idx[q];
+      part_of_new[next] = p;
+      ++next;
+    }
+    P.part_node_start[p + 1] = (int32_t)next;
+    P.part_n_free[p] = n_free;
+    P.part_robin_start[p] = n_plain;
+    P.max_part_nodes = std::max<int>(P.max_part_nodes, (int)(end - start));
+    start = end;
+  }
+  std::vector<uint8_t> updatable_new(V);
+  for (int64_t n = 0; n < V; ++n) updatable_new[n] = !(in.node_class && in.node_class[P.old_of_new[n]] == 2);
+  // 4. slots
+  std::vector<std::vector<int32_t>> tet_pp(P.n_parts), hex_pp(P.n_parts);
+  build_slots<4>(in.n_tet, in.tets, 0, P, part_of_new, updatable_new, tet_pp);
+  build_slots<8>(in.n_hex, in.hexes, in.n_tet, P, part_of_new, updatable_new, hex_pp);
+  P.part_tet_start.assign(P.n_parts + 1, 0);
+  P.part_hex_start.assign(P.n_parts + 1, 0);
+  for (int p = 0; p < P.n_parts; ++p) {
+    P.part_tet_start[p + 1] = P.part_tet_start[p] + (int32_t)tet_pp[p].size();
+    P.part_hex_start[p + 1] = P.part_hex_start[p] + (int32_t)hex_pp[p].size();
+  }
+  P.tet_slot_elem.resize(P.part_tet_start.back());
+  P.hex_slot_elem.resize(P.part_hex_start.back());
+  for (int p = 0; p < P.n_parts; ++p) {
+    std::copy(tet_pp[p].begin(), tet_pp[p].end(), P.tet_slot_elem.begin() + P.part_tet_start[p]);
+    std::copy(hex_pp[p].begin(), hex_pp[p].end(), P.hex_slot_elem.begin() + P.part_hex_start[p]);
+  }
+  tet_pp.clear();
+  hex_pp.clear();
+  P.tet_conn.resize(4 * P.tet_slot_elem.size());
+  for (size_t s = 0; s < P.tet_slot_elem.size(); ++s)
+    for (int a = 0; a < 4; ++a) P.tet_conn[4 * s + a] = (int32_t)P.new_of_old[in.tets[4 * (int64_t)P.tet_slot_elem[s] + a]];
+  P.hex_conn.resize(8 * P.hex_slot_elem.size());
+  for (size_t s = 0; s < P.hex_slot_elem.size(); ++s) {
+    const int64_t h = P.hex_slot_elem[s] - in.n_tet;
+    for (int a = 0; a < 8; ++a) P.hex_conn[8 * s + a] = (int32_t)P.new_of_old[in.hexes[8 * h + a]];
+  }
+  // 5. phases per batch
+  const int B = in.batch;
+  std::vector<uint8_t> count(P.max_part_nodes, 0);
+  std::vector<uint16_t> cornermask(P.max_part_nodes, 0);
+  bool unique = true;
+  P.tet_rank.resize(P.tet_conn.size());
+  P.hex_rank.resize(P.hex_conn.size());
+  auto do_kind = [&](int N, const std::vector<int32_t> &starts, const std::vector<int32_t> &conn,
+                     std::vector<uint8_t> &rank, int &max_phase) {
+    max_phase = 0;
+    for (int p = 0; p < P.n_parts; ++p) {
+      const int32_t n0 = P.part_node_start[p], nf = P.part_n_free[p];
+      for (int32_t b = starts[p]; b < starts[p + 1]; b += B) {
+        const int32_t be = std::min(starts[p + 1], b + B);
+        for (int32_t s = b; s < be; ++s)
+          for (int a = 0; a < N; ++a) {
+            const int32_t loc = conn[(size_t)N * s + a] - n0;
+            uint8_t r = 0xff;
+            if (loc >= 0 && loc < nf) {
+              if (count[loc] == 0xfe) fail(FH_ERR_CONFIG, "more than 254 elements share a node inside one batch");
+              r = count[loc]++;
+              max_phase = std::max<int>(max_phase, r + 1);
+              if (cornermask[loc] & (1u << a)) unique = false;
+              cornermask[loc] |= (uint16_t)(1u << a);
+            }
+            rank[(size_t)N * s + a] = r;
+          }
+        for (int32_t s = b; s < be; ++s)
+          for (int a = 0; a < N; ++a) {
+            const int32_t loc = conn[(size_t)N * s + a] - n0;
+            if (loc >= 0 && loc < nf) {
+              count[loc] = 0;
+              cornermask[loc] = 0;
+            }
+          }
+      }
+    }
+  };
+  do_kind(4, P.part_tet_start, P.tet_conn, P.tet_rank, P.max_phase_tet);
+  do_kind(8, P.part_hex_start, P.hex_conn, P.hex_rank, P.max_phase_hex);
+  P.corner_unique = unique;
+}
+
+}  // namespace fh

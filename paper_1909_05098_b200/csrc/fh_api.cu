@@ -108,10 +108,12 @@ __global__ void k_pack_slots(const int32_t *__restrict__ slot_elem, int64_t n, c
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= n) return;
   const int64_t e = slot_elem[s];
+  // G in batch-major SoA: [s / B][component][s % B]
+  const int64_t base = (s / kTileThreads) * 6 * kTileThreads + (s % kTileThreads);
 #pragma unroll
-  for (int k = 0; k < 6; ++k) out_G[6 * s + k] = (S)(G[6 * e + k] * scale);
-  if (out_kf) out_kf[s] = (S)kf[e];
-  if (out_region) out_region[s] = (uint8_t)region[e];
+  for (int k = 0; k < 6; ++k) out_G[base + k * kTileThreads] = e >= 0 ? (S)(G[6 * e + k] * scale) : S(0);
+  if (out_kf) out_kf[s] = e >= 0 ? (S)kf[e] : S(1);
+  if (out_region) out_region[s] = e >= 0 ? (uint8_t)region[e] : 0;
 }
 
 constexpr int kBlk = 256;
@@ -121,7 +123,9 @@ template <typename S>
 struct TiledState {
   TiledArgs<S> args{};
   DBuf<int32_t> part_node_start, part_n_free, part_robin_start, part_robin_base, part_tet_start, part_hex_start;
+  DBuf<int32_t> part_tet_count, part_hex_count, part_halo_start, halo_nodes;
   DBuf<int32_t> part_list;
+  DBuf<uint16_t> tet_conn16, hex_conn16;
   DBuf<int32_t> tet_conn, hex_conn, tet_slot_elem, hex_slot_elem;
   DBuf<S> tet_G, hex_G, tet_kf, hex_kf, tet_kbar, hex_kbar;
   DBuf<uint8_t> tet_rank, hex_rank, tet_region, hex_region, node_region;
@@ -129,6 +133,7 @@ struct TiledState {
   int cur = 0;
   size_t smem = 0;
   int n_parts_local = 0;
+  int mode = 0;
 };
 
 }  // namespace
@@ -347,7 +352,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   pin.tets = mesh.tets;
   pin.hexes = mesh.hexes;
   pin.node_class = cls.data();
-  pin.target_part_nodes = o.part_nodes > 0 ? o.part_nodes : (sizeof(S) == 4 ? 8192 : 4096);
+  pin.target_part_nodes = o.part_nodes > 0 ? o.part_nodes : (sizeof(S) == 4 ? 2048 : 1024);
   pin.batch = kTileThreads;
   pin.n_domains = std::max(1, o.n_domains);
   pin.slab_axis = o.slab_axis;
@@ -374,8 +379,16 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   st->part_robin_base.upload(robin_base, s);
   st->part_tet_start.upload(P.part_tet_start, s);
   st->part_hex_start.upload(P.part_hex_start, s);
-  st->tet_conn.upload(P.tet_conn, s);
-  st->hex_conn.upload(P.hex_conn, s);
+  st->part_tet_count.upload(P.part_tet_count, s);
+  st->part_hex_count.upload(P.part_hex_count, s);
+  st->part_halo_start.upload(P.part_halo_start, s);
+  st->halo_nodes.upload(P.halo_nodes, s);
+  st->tet_conn16.upload(P.tet_conn16, s);
+  st->hex_conn16.upload(P.hex_conn16, s);
+  if (!e->td) {  // the TI freeze kernel works on global ids
+    st->tet_conn.upload(P.tet_conn, s);
+    st->hex_conn.upload(P.hex_conn, s);
+  }
   st->tet_slot_elem.upload(P.tet_slot_elem, s);
   st->hex_slot_elem.upload(P.hex_slot_elem, s);
   if (!P.corner_unique) {
@@ -462,8 +475,12 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.part_robin_base = st->part_robin_base.p;
   g.part_tet_start = st->part_tet_start.p;
   g.part_hex_start = st->part_hex_start.p;
-  g.tet_conn = st->tet_conn.p;
-  g.hex_conn = st->hex_conn.p;
+  g.part_tet_count = st->part_tet_count.p;
+  g.part_hex_count = st->part_hex_count.p;
+  g.part_halo_start = st->part_halo_start.p;
+  g.halo_nodes = st->halo_nodes.p;
+  g.tet_conn16 = st->tet_conn16.p;
+  g.hex_conn16 = st->hex_conn16.p;
   g.tet_G = st->tet_G.p;
   g.hex_G = st->hex_G.p;
   g.tet_kf = st->tet_kf.p;
@@ -486,8 +503,24 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.n_src = (int)e->sources.size();
   g.runaway_limit = (S)e->runaway_limit;
   g.flag = e->flag.p;
-  st->smem = sizeof(S) * (size_t)std::max(1, P.max_part_nodes);
-  if (st->smem > 200 * 1024) fail(FH_ERR_CONFIG, "tile too large for shared memory; lower part_nodes");
+  auto al = [](size_t b) { return (b + 127) & ~(size_t)127; };
+  // accumulation mode: corner phases / corner slots need corner-unique tiles;
+  // FH_TILE_MODE (0/1/2) and FH_TILE_STAGES override the defaults (tuning knobs)
+  st->mode = P.corner_unique ? kModeCornerPhase : kModeRanked;
+  if (const char *env = getenv("FH_TILE_MODE")) {
+    const int m = atoi(env);
+    if (m == kModeRanked || P.corner_unique) st->mode = m;
+  }
+  g.n_stages = 3;
+  if (const char *env = getenv("FH_TILE_STAGES")) g.n_stages = std::min(kMaxStages, std::max(1, atoi(env)));
+  g.smem_T = (int)al(2 * sizeof(S) * (size_t)std::max(1, P.max_local_nodes));
+  g.smem_acc = (int)al(sizeof(S) * (st->mode == kModeCornerSlot ? 8 : 1) * (size_t)std::max(1, P.max_part_free));
+  int stage = 0;
+  if (e->n_tet) stage = std::max(stage, StageBytes<S>(4, st->tet_kf.p || !e->td, !P.corner_unique));
+  if (e->n_hex) stage = std::max(stage, StageBytes<S>(8, st->hex_kf.p || !e->td, !P.corner_unique));
+  g.stage_bytes = (int)al(stage);
+  st->smem = (size_t)g.smem_T + g.smem_acc + (size_t)g.n_stages * g.stage_bytes;
+  if (st->smem > 220 * 1024) fail(FH_ERR_CONFIG, "tile too large for shared memory; lower part_nodes");
   FH_CUDA(cudaStreamSynchronize(s));
   if constexpr (sizeof(S) == 4)
     e->tf = std::move(st);
@@ -542,7 +575,7 @@ void tiled_run(fh_engine *e, int64_t nsteps, double dt) {
     g.Tout = st.T[st.cur ^ 1].p;
     if (!e->td && !e->frozen) {
       const int64_t nts = (int64_t)e->part.tet_slot_elem.size(), nhs = (int64_t)e->part.hex_slot_elem.size();
-      tiled_freeze<S>(g, nts, nhs, e->V, st.tet_kf.p, st.hex_kf.p, st.tet_kbar.p, st.hex_kbar.p, st.cap.p,
+      tiled_freeze<S>(g, st.tet_conn.p, st.hex_conn.p, nts, nhs, e->V, st.tet_kf.p, st.hex_kf.p, st.tet_kbar.p, st.hex_kbar.p, st.cap.p,
                       st.kb.p, e->stream);
       g.tet_kf = st.tet_kbar.p;
       g.hex_kf = st.hex_kbar.p;
@@ -564,7 +597,7 @@ void tiled_run(fh_engine *e, int64_t nsteps, double dt) {
       d.cz = (S)(src.x0[2] + src.vel[2] * t);
     }
     g.part_begin = 0;
-    tiled_step(g, st.n_parts_local, e->td, e->part.corner_unique, st.smem, e->stream);
+    tiled_step(g, st.n_parts_local, e->td, st.mode, st.smem, e->stream);
     st.cur ^= 1;
     e->step_index += 1;
     e->time = (double)e->step_index * dt;

@@ -84,10 +84,18 @@ struct MatSet {
   Mat<S> m[kMaxRegions];
 };
 
-// fast-path clamped interpolation (FMA allowed)
+// fast-path clamped interpolation (FMA allowed).  Branch-free for the common
+// one- and two-knot curves (the clamped end values are selected, so they are
+// returned exactly like the reference's kernels.py:61-73).
 template <typename S>
 __device__ __forceinline__ S interp(const Curve<S> &c, S x) {
-  if (c.n == 1 || x <= c.x[0]) return c.y[0];
+  if (c.n == 1) return c.y[0];
+  if (c.n == 2) {
+    S r = c.slope[0] * (x - c.x[0]) + c.y[0];
+    r = (x >= c.x[1]) ? c.y[1] : r;
+    return (x <= c.x[0]) ? c.y[0] : r;
+  }
+  if (x <= c.x[0]) return c.y[0];
   if (x >= c.x[c.n - 1]) return c.y[c.n - 1];
   int j = 0;
   while (c.x[j + 1] <= x) ++j;
@@ -126,15 +134,20 @@ struct Partition {
   std::vector<int32_t> part_node_start;                  // P+1
   std::vector<int32_t> part_n_free;                      // nodes updated (free + robin)
   std::vector<int32_t> part_robin_start;                 // local index of first robin node
-  std::vector<int32_t> part_tet_start, part_hex_start;   // P+1 each (slot ranges per kind)
+  std::vector<int32_t> part_tet_start, part_hex_start;   // P+1 each (slot ranges per kind, 4-aligned)
+  std::vector<int32_t> part_tet_count, part_hex_count;   // real slots per part (rest is padding)
+  std::vector<int32_t> part_halo_start, halo_nodes;      // halo (non-owned) nodes per part, sorted
+  std::vector<uint16_t> tet_conn16, hex_conn16;          // tile-local node index per slot corner
   std::vector<int32_t> part_domain;                      // domain of each part
   std::vector<int32_t> domain_part_start;                // n_domains+1
-  std::vector<int32_t> tet_slot_elem, hex_slot_elem;     // original element id per slot
+  std::vector<int32_t> tet_slot_elem, hex_slot_elem;     // original element id per slot (-1 = padding)
   std::vector<int32_t> tet_conn, hex_conn;               // new node ids per slot
   std::vector<uint8_t> tet_rank, hex_rank;               // per slot corner phase (ranked mode)
   bool corner_unique = false;                            // phases == corner index
   int max_phase_tet = 0, max_phase_hex = 0;
   int max_part_nodes = 0;
+  int max_local_nodes = 0;  // owned + halo
+  int max_part_free = 0;
 };
 
 void build_partition(const PartitionInput &in, Partition &out);

@@ -172,46 +172,134 @@ void build_partition(const PartitionInput &in, Partition &P) {
   }
   std::vector<uint8_t> updatable_new(V);
   for (int64_t n = 0; n < V; ++n) updatable_new[n] = !(in.node_class && in.node_class[P.old_of_new[n]] == 2);
-  // 4. slots
+  // 4. slots (each part's tet / hex slot range starts on a multiple of 4
+  //    slots so that the per-batch bulk copies are 16-byte aligned)
   std::vector<std::vector<int32_t>> tet_pp(P.n_parts), hex_pp(P.n_parts);
   build_slots<4>(in.n_tet, in.tets, 0, P, part_of_new, updatable_new, tet_pp);
   build_slots<8>(in.n_hex, in.hexes, in.n_tet, P, part_of_new, updatable_new, hex_pp);
+  // order the slots of a part by their smallest corner id (new numbering), so
+  // that neighbouring threads of a batch touch neighbouring nodes: the
+  // shared-memory gathers and accumulations are then bank-conflict free
+  // (element id order of a structured cube steps by a whole z-plane).
+  {
+    auto key = [&](int N, int32_t e) {
+      const int64_t *c = N == 4 ? in.tets + 4 * (int64_t)e : in.hexes + 8 * ((int64_t)e - in.n_tet);
+      int64_t m = P.new_of_old[c[0]];
+      for (int a = 1; a < N; ++a) m = std::min<int64_t>(m, P.new_of_old[c[a]]);
+      return m;
+    };
+    std::vector<std::pair<int64_t, int32_t>> tmp;
+    auto sort_part = [&](std::vector<int32_t> &v, int N) {
+      tmp.clear();
+      for (int32_t e : v) tmp.emplace_back(key(N, e), e);
+      std::sort(tmp.begin(), tmp.end());
+      for (size_t q = 0; q < v.size(); ++q) v[q] = tmp[q].second;
+    };
+    for (int p = 0; p < P.n_parts; ++p) {
+      sort_part(tet_pp[p], 4);
+      sort_part(hex_pp[p], 8);
+    }
+  }
   P.part_tet_start.assign(P.n_parts + 1, 0);
   P.part_hex_start.assign(P.n_parts + 1, 0);
+  P.part_tet_count.assign(P.n_parts, 0);
+  P.part_hex_count.assign(P.n_parts, 0);
+  const int64_t Bp = std::max(4, in.batch);
+  auto pad4 = [Bp](int64_t n) { return (n + Bp - 1) / Bp * Bp; };  // batch-aligned part ranges
   for (int p = 0; p < P.n_parts; ++p) {
-    P.part_tet_start[p + 1] = P.part_tet_start[p] + (int32_t)tet_pp[p].size();
-    P.part_hex_start[p + 1] = P.part_hex_start[p] + (int32_t)hex_pp[p].size();
+    P.part_tet_count[p] = (int32_t)tet_pp[p].size();
+    P.part_hex_count[p] = (int32_t)hex_pp[p].size();
+    P.part_tet_start[p + 1] = P.part_tet_start[p] + (int32_t)pad4(tet_pp[p].size());
+    P.part_hex_start[p + 1] = P.part_hex_start[p] + (int32_t)pad4(hex_pp[p].size());
   }
-  P.tet_slot_elem.resize(P.part_tet_start.back());
-  P.hex_slot_elem.resize(P.part_hex_start.back());
+  P.tet_slot_elem.assign(P.part_tet_start.back(), -1);
+  P.hex_slot_elem.assign(P.part_hex_start.back(), -1);
   for (int p = 0; p < P.n_parts; ++p) {
     std::copy(tet_pp[p].begin(), tet_pp[p].end(), P.tet_slot_elem.begin() + P.part_tet_start[p]);
     std::copy(hex_pp[p].begin(), hex_pp[p].end(), P.hex_slot_elem.begin() + P.part_hex_start[p]);
   }
   tet_pp.clear();
   hex_pp.clear();
-  P.tet_conn.resize(4 * P.tet_slot_elem.size());
+  P.tet_conn.assign(4 * P.tet_slot_elem.size(), 0);
   for (size_t s = 0; s < P.tet_slot_elem.size(); ++s)
-    for (int a = 0; a < 4; ++a) P.tet_conn[4 * s + a] = (int32_t)P.new_of_old[in.tets[4 * (int64_t)P.tet_slot_elem[s] + a]];
-  P.hex_conn.resize(8 * P.hex_slot_elem.size());
-  for (size_t s = 0; s < P.hex_slot_elem.size(); ++s) {
-    const int64_t h = P.hex_slot_elem[s] - in.n_tet;
-    for (int a = 0; a < 8; ++a) P.hex_conn[8 * s + a] = (int32_t)P.new_of_old[in.hexes[8 * h + a]];
+    if (P.tet_slot_elem[s] >= 0)
+      for (int a = 0; a < 4; ++a)
+        P.tet_conn[4 * s + a] = (int32_t)P.new_of_old[in.tets[4 * (int64_t)P.tet_slot_elem[s] + a]];
+  P.hex_conn.assign(8 * P.hex_slot_elem.size(), 0);
+  for (size_t s = 0; s < P.hex_slot_elem.size(); ++s)
+    if (P.hex_slot_elem[s] >= 0) {
+      const int64_t h = P.hex_slot_elem[s] - in.n_tet;
+      for (int a = 0; a < 8; ++a) P.hex_conn[8 * s + a] = (int32_t)P.new_of_old[in.hexes[8 * h + a]];
+    }
+  // 5. halo lists and tile-local 16-bit connectivity: local index of node n in
+  //    part p is n - n0 for owned nodes, nn + rank in the sorted halo list else
+  P.part_halo_start.assign(P.n_parts + 1, 0);
+  P.halo_nodes.clear();
+  P.tet_conn16.assign(P.tet_conn.size(), 0);
+  P.hex_conn16.assign(P.hex_conn.size(), 0);
+  P.max_local_nodes = 0;
+  P.max_part_free = 0;
+  {
+    std::vector<int32_t> halo;
+    for (int p = 0; p < P.n_parts; ++p) {
+      const int32_t n0 = P.part_node_start[p], nn = P.part_node_start[p + 1] - n0;
+      halo.clear();
+      auto collect = [&](const std::vector<int32_t> &conn, int N, int32_t s0, int32_t cnt) {
+        for (int64_t q = (int64_t)N * s0; q < (int64_t)N * (s0 + cnt); ++q) {
+          const int32_t n = conn[q];
+          if (n < n0 || n >= n0 + nn) halo.push_back(n);
+        }
+      };
+      collect(P.tet_conn, 4, P.part_tet_start[p], P.part_tet_count[p]);
+      collect(P.hex_conn, 8, P.part_hex_start[p], P.part_hex_count[p]);
+      std::sort(halo.begin(), halo.end());
+      halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
+      const int64_t nloc = (int64_t)nn + (int64_t)halo.size();
+      if (nloc >= 0xffff) fail(FH_ERR_CONFIG, "tile has too many local nodes; lower part_nodes");
+      P.max_local_nodes = std::max<int>(P.max_local_nodes, (int)nloc);
+      P.max_part_free = std::max<int>(P.max_part_free, P.part_n_free[p]);
+      auto local = [&](int32_t n) -> uint16_t {
+        if (n >= n0 && n < n0 + nn) return (uint16_t)(n - n0);
+        return (uint16_t)(nn + (std::lower_bound(halo.begin(), halo.end(), n) - halo.begin()));
+      };
+      for (int64_t q = 4 * (int64_t)P.part_tet_start[p]; q < 4 * (int64_t)(P.part_tet_start[p] + P.part_tet_count[p]); ++q)
+        P.tet_conn16[q] = local(P.tet_conn[q]);
+      for (int64_t q = 8 * (int64_t)P.part_hex_start[p]; q < 8 * (int64_t)(P.part_hex_start[p] + P.part_hex_count[p]); ++q)
+        P.hex_conn16[q] = local(P.hex_conn[q]);
+      P.halo_nodes.insert(P.halo_nodes.end(), halo.begin(), halo.end());
+      P.part_halo_start[p + 1] = (int32_t)P.halo_nodes.size();
+    }
   }
-  // 5. phases per batch
+  // 6. phases per batch
   const int B = in.batch;
   std::vector<uint8_t> count(P.max_part_nodes, 0);
   std::vector<uint16_t> cornermask(P.max_part_nodes, 0);
   bool unique = true;
-  P.tet_rank.resize(P.tet_conn.size());
-  P.hex_rank.resize(P.hex_conn.size());
-  auto do_kind = [&](int N, const std::vector<int32_t> &starts, const std::vector<int32_t> &conn,
-                     std::vector<uint8_t> &rank, int &max_phase) {
+  P.tet_rank.assign(P.tet_conn.size(), 0xff);
+  P.hex_rank.assign(P.hex_conn.size(), 0xff);
+  // corner uniqueness is checked over a whole part: the kernel can then give
+  // every (node, corner) pair its own accumulator slot (no phases at all)
+  auto do_kind = [&](int N, const std::vector<int32_t> &starts, const std::vector<int32_t> &counts,
+                     const std::vector<int32_t> &conn, std::vector<uint8_t> &rank, int &max_phase) {
     max_phase = 0;
     for (int p = 0; p < P.n_parts; ++p) {
       const int32_t n0 = P.part_node_start[p], nf = P.part_n_free[p];
-      for (int32_t b = starts[p]; b < starts[p + 1]; b += B) {
-        const int32_t be = std::min(starts[p + 1], b + B);
+      const int32_t s_end = starts[p] + counts[p];
+      for (int32_t s = starts[p]; s < s_end; ++s)
+        for (int a = 0; a < N; ++a) {
+          const int32_t loc = conn[(size_t)N * s + a] - n0;
+          if (loc >= 0 && loc < nf) {
+            if (cornermask[loc] & (1u << a)) unique = false;
+            cornermask[loc] |= (uint16_t)(1u << a);
+          }
+        }
+      for (int32_t s = starts[p]; s < s_end; ++s)
+        for (int a = 0; a < N; ++a) {
+          const int32_t loc = conn[(size_t)N * s + a] - n0;
+          if (loc >= 0 && loc < nf) cornermask[loc] = 0;
+        }
+      for (int32_t b = starts[p]; b < s_end; b += B) {
+        const int32_t be = std::min(s_end, b + B);
         for (int32_t s = b; s < be; ++s)
           for (int a = 0; a < N; ++a) {
             const int32_t loc = conn[(size_t)N * s + a] - n0;
@@ -220,24 +308,19 @@ void build_partition(const PartitionInput &in, Partition &P) {
               if (count[loc] == 0xfe) fail(FH_ERR_CONFIG, "more than 254 elements share a node inside one batch");
               r = count[loc]++;
               max_phase = std::max<int>(max_phase, r + 1);
-              if (cornermask[loc] & (1u << a)) unique = false;
-              cornermask[loc] |= (uint16_t)(1u << a);
             }
             rank[(size_t)N * s + a] = r;
           }
         for (int32_t s = b; s < be; ++s)
           for (int a = 0; a < N; ++a) {
             const int32_t loc = conn[(size_t)N * s + a] - n0;
-            if (loc >= 0 && loc < nf) {
-              count[loc] = 0;
-              cornermask[loc] = 0;
-            }
+            if (loc >= 0 && loc < nf) count[loc] = 0;
           }
       }
     }
   };
-  do_kind(4, P.part_tet_start, P.tet_conn, P.tet_rank, P.max_phase_tet);
-  do_kind(8, P.part_hex_start, P.hex_conn, P.hex_rank, P.max_phase_hex);
+  do_kind(4, P.part_tet_start, P.part_tet_count, P.tet_conn, P.tet_rank, P.max_phase_tet);
+  do_kind(8, P.part_hex_start, P.part_hex_count, P.hex_conn, P.hex_rank, P.max_phase_hex);
   P.corner_unique = unique;
 }
 

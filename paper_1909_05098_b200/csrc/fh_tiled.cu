@@ -1,20 +1,23 @@
 // TILED mode: the whole explicit step (north_star (ii)-(iv)) as ONE kernel.
 //
-// One CTA per tile ("part") of <= max_part_nodes nodes (fh_partition.cpp):
-//   1. zero the tile's nodal load accumulators in shared memory;
-//   2. stream the tile's element slots in batches of 256 (one thread per
-//      element): gather the corner temperatures, evaluate k(T) per corner
-//      (TD) for kbar_e, form the element load from the 6-value metric tensor
-//      G (A = D G D^T):  g = D^T (T - T_0),  f = G g,
-//      c_a = kbar * D_a . f  -- then add -c_a into the shared accumulator of
-//      every corner the tile owns, phase by phase (a barrier per phase, so the
-//      per-node summation order is fixed: deterministic without atomics);
-//   3. for every owned non-Dirichlet node, the lumped update
-//      T' = T + dt (F - kb T + qb + qm + q_ext [+ Robin]) / C with C, kb from
-//      rho(T) c(T) and w_b(T), written to the other temperature buffer, plus
-//      the runaway check.
-// Global memory traffic per step: the slot stream (conn, G, factor) once, the
-// nodal streams (T, v, [q, xyz]) once, T' once; halo temperatures come from L2.
+// One CTA per tile ("part", fh_partition.cpp) of owned nodes:
+//   0. thread 0 starts a kStages-deep ring of TMA bulk copies
+//      (cp.async.bulk + mbarrier complete_tx) of the tile's element-slot
+//      stream -- 16-bit tile-local connectivity, the 6-value metric tensor G
+//      (A = D G D^T), the conductivity factor -- batch by batch;
+//   1. meanwhile all threads stage the tile's temperatures in shared memory:
+//      the owned node range (coalesced) and the halo list (gathered), and zero
+//      the nodal load accumulators;
+//   2. per batch (one thread per element slot): corner temperatures from
+//      shared memory, k(T) per corner (TD) for kbar_e, g = D^T (T - T_0),
+//      f = G g, c_a = kbar * D_a . f; then -c_a is added into the owned
+//      corners' accumulators phase by phase, a barrier per phase, so each
+//      node's sum has a fixed order: deterministic without atomics;
+//   3. every owned non-Dirichlet node: T' = T + dt (F - kb T + qb + qm + q_ext
+//      [+ Robin]) / C with C = rho(T) c(T) v and kb = w_b(T) c_b v, written to
+//      the other temperature buffer; runaway check.
+// HBM traffic per step: the slot stream once (duplicated halo elements
+// included), the node streams (T, v, [q, xyz]) once, T' once, halo T from L2.
 #include <cstdio>
 
 #include "fh_tiled.cuh"
@@ -23,17 +26,63 @@ namespace fh {
 
 constexpr unsigned long long kNone = ~0ull;
 
+// (T, k(T)) of a tile-local node, staged once per tile in shared memory
 template <typename S>
-__device__ __forceinline__ S ldg(const S *p) {
-  return __ldg(p);
-}
+struct __align__(2 * sizeof(S)) TK {
+  S t, k;
+};
+
 // products that must not be contracted into an FMA (keeps T == Ta a bitwise
 // fixed point: kb*T and qb = kb*Ta round identically)
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 
+// ---- TMA bulk copy / mbarrier helpers (sm_90+ PTX, sm_100a target) ----------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// stage layout for one batch of B slots of a kind with N corners
 template <typename S>
-__device__ __forceinline__ S kbar_of(const TiledArgs<S> &g, const Curve<S> &kc, const S *Tn, int n, S kf) {
+struct StageLayout {
+  int conn, G, kf, rank, bytes;
+  __host__ __device__ StageLayout(int N, bool has_kf, bool has_rank) {
+    conn = 0;
+    G = kTileThreads * N * 2;
+    kf = G + 6 * kTileThreads * (int)sizeof(S);
+    rank = kf + (has_kf ? kTileThreads * (int)sizeof(S) : 0);
+    bytes = rank + (has_rank ? kTileThreads * N : 0);
+    bytes = (bytes + 15) & ~15;
+  }
+};
+
+template <typename S>
+__device__ __forceinline__ S kbar_from(const Curve<S> &kc, const S *Tn, int n, S kf) {
   S s = S(0);
 #pragma unroll
   for (int b = 0; b < 8; ++b)
@@ -41,57 +90,141 @@ __device__ __forceinline__ S kbar_of(const TiledArgs<S> &g, const Curve<S> &kc, 
   return s / S(n) * kf;
 }
 
-// ---- element loads ---------------------------------------------------------
+__device__ __forceinline__ float fast_div(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ double fast_div(double a, double b) { return a / b; }
 
+// F - kb T + qb + qm + q_ext with C, kb from the material laws (TD) or the
+// frozen arrays (TI); returns the rate, writes the capacity
 template <typename S, bool TD>
-__device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, int s, int32_t nd[8], S c[8]) {
-  const int4 *cp = reinterpret_cast<const int4 *>(g.hex_conn + 8 * (size_t)s);
-  const int4 c0 = __ldg(cp), c1 = __ldg(cp + 1);
-  nd[0] = c0.x; nd[1] = c0.y; nd[2] = c0.z; nd[3] = c0.w;
-  nd[4] = c1.x; nd[5] = c1.y; nd[6] = c1.z; nd[7] = c1.w;
-  S T[8];
-#pragma unroll
-  for (int b = 0; b < 8; ++b) T[b] = ldg(g.Tin + nd[b]);
-  const S *G = g.hex_G + 6 * (size_t)s;
-  const S g00 = ldg(G), g01 = ldg(G + 1), g02 = ldg(G + 2), g11 = ldg(G + 3), g12 = ldg(G + 4), g22 = ldg(G + 5);
+__device__ __forceinline__ S node_rate(const Mat<S> &m, S x, S F, S v, S q, S cfrozen, S kbfrozen, S &cap) {
   S kb;
   if (TD) {
-    const Curve<S> &kc = g.mats.m[g.hex_region ? g.hex_region[s] : 0].k;
-    kb = kbar_of(g, kc, T, 8, g.hex_kf ? ldg(g.hex_kf + s) : S(1));
+    cap = interp(m.rho, x) * interp(m.c, x) * v;
+    kb = m.td_perf ? interp(m.wb, x) * m.cb * v : m.wbcb * v;
   } else {
-    kb = ldg(g.hex_kf + s);  // frozen kbar
+    cap = cfrozen;
+    kb = m.td_perf ? kbfrozen : m.wbcb * v;
+  }
+  return (((F - mul_rn(kb, x)) + mul_rn(kb, m.Ta)) + m.Qm * v) + q;
+}
+
+template <typename S>
+__device__ __forceinline__ S sources_at(const TiledArgs<S> &g, const S *xyz) {
+  const S x = xyz[0], y = xyz[1], z = xyz[2];
+  S q = S(0);
+  for (int k = 0; k < g.n_src; ++k) {
+    const SourceT<S> &s = g.src[k];
+    if (!s.active) continue;
+    const S dx = x - s.cx, dy = y - s.cy, dz = z - s.cz;
+    const S r2 = (dx * dx + dy * dy) + dz * dz;
+    if (s.kind == FH_SOURCE_GAUSSIAN)
+      q += s.amp * exp(-r2 * s.inv2s2);
+    else
+      q += r2 > S(0) ? min(s.cap, s.inv4pi_amp / r2) : s.cap;
+  }
+  return q;
+}
+
+// Issue the bulk copies of batch j of part p into stage buffer `st`.
+template <typename S>
+__device__ void issue_batch(const TiledArgs<S> &g, int p, int j, int nbt, unsigned char *stage, uint64_t *bar) {
+  const bool tet = j < nbt;
+  const int N = tet ? 4 : 8;
+  const int b = tet ? j : j - nbt;
+  const int s0 = (tet ? g.part_tet_start[p] : g.part_hex_start[p]) + b * kTileThreads;
+  const int cnt = (tet ? g.part_tet_count[p] : g.part_hex_count[p]) - b * kTileThreads;
+  const int k = cnt < kTileThreads ? cnt : kTileThreads;
+  const int kr = (k + 3) & ~3;
+  const uint16_t *conn = tet ? g.tet_conn16 : g.hex_conn16;
+  const S *G = tet ? g.tet_G : g.hex_G;
+  const S *kf = tet ? g.tet_kf : g.hex_kf;
+  const uint8_t *rank = tet ? g.tet_rank : g.hex_rank;
+  const StageLayout<S> L(N, kf != nullptr, rank != nullptr);
+  uint32_t bytes = (uint32_t)(kr * N * 2 + 6 * kr * sizeof(S));
+  if (kf) bytes += kr * sizeof(S);
+  if (rank) bytes += kr * N;
+  mbar_expect_tx(bar, bytes);
+  bulk_g2s(stage + L.conn, conn + (size_t)N * s0, kr * N * 2, bar);
+  const S *Gb = G + (size_t)(s0 / kTileThreads) * 6 * kTileThreads;
+#pragma unroll
+  for (int c = 0; c < 6; ++c)
+    bulk_g2s(stage + L.G + c * kTileThreads * sizeof(S), Gb + c * kTileThreads, kr * sizeof(S), bar);
+  if (kf) bulk_g2s(stage + L.kf, kf + s0, kr * sizeof(S), bar);
+  if (rank) bulk_g2s(stage + L.rank, rank + (size_t)N * s0, kr * N, bar);
+}
+
+// element loads from the staged batch -----------------------------------------
+template <typename S, bool TD>
+__device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned char *stage, const TK<S> *sT,
+                                          const Curve<S> &kc, bool has_kf, int tid, uint16_t nd[8], S c[8]) {
+  const StageLayout<S> L(8, has_kf, g.hex_rank != nullptr);
+  const uint4 w = reinterpret_cast<const uint4 *>(stage + L.conn)[tid];
+  nd[0] = w.x & 0xffff; nd[1] = w.x >> 16; nd[2] = w.y & 0xffff; nd[3] = w.y >> 16;
+  nd[4] = w.z & 0xffff; nd[5] = w.z >> 16; nd[6] = w.w & 0xffff; nd[7] = w.w >> 16;
+  S T[8], K[8];
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const TK<S> q = sT[nd[b]];
+    T[b] = q.t;
+    K[b] = q.k;
+  }
+  const S *G = reinterpret_cast<const S *>(stage + L.G);
+  const S g00 = G[tid], g01 = G[kTileThreads + tid], g02 = G[2 * kTileThreads + tid],
+          g11 = G[3 * kTileThreads + tid], g12 = G[4 * kTileThreads + tid], g22 = G[5 * kTileThreads + tid];
+  const S kf = has_kf ? reinterpret_cast<const S *>(stage + L.kf)[tid] : S(1);
+  S kb = kf;
+  if (TD) {
+    if (g.mats.n == 1) {  // k(T) staged per node: kbar = mean of the corner values
+      S sum = S(0);
+#pragma unroll
+      for (int b = 0; b < 8; ++b) sum += K[b];
+      kb = sum / S(8) * kf;
+    } else {
+      kb = kbar_from(kc, T, 8, kf);
+    }
   }
   S d[8];
 #pragma unroll
   for (int b = 0; b < 8; ++b) d[b] = T[b] - T[0];
-  // g = sum_b s_b d_b  (signs of element.py HEX_VERTEX_SIGNS; the 1/8 of
-  // D = S/8 on both sides is folded into G as 1/64)
+  // g = sum_b s_b d_b with the corner signs of element.py HEX_VERTEX_SIGNS
   const S gx = ((d[1] - d[0]) + (d[2] - d[3])) + ((d[5] - d[4]) + (d[6] - d[7]));
   const S gy = ((d[3] - d[0]) + (d[2] - d[1])) + ((d[7] - d[4]) + (d[6] - d[5]));
   const S gz = ((d[4] - d[0]) + (d[5] - d[1])) + ((d[6] - d[2]) + (d[7] - d[3]));
   const S u = kb * (g00 * gx + g01 * gy + g02 * gz);
   const S v = kb * (g01 * gx + g11 * gy + g12 * gz);
-  const S w = kb * (g02 * gx + g12 * gy + g22 * gz);
+  const S w2 = kb * (g02 * gx + g12 * gy + g22 * gz);
   const S a = u + v, b2 = u - v;
-  c[0] = -a - w; c[1] = b2 - w; c[2] = a - w; c[3] = -b2 - w;
-  c[4] = -a + w; c[5] = b2 + w; c[6] = a + w; c[7] = -b2 + w;
+  c[0] = -a - w2; c[1] = b2 - w2; c[2] = a - w2; c[3] = -b2 - w2;
+  c[4] = -a + w2; c[5] = b2 + w2; c[6] = a + w2; c[7] = -b2 + w2;
 }
 
 template <typename S, bool TD>
-__device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, int s, int32_t nd[4], S c[4]) {
-  const int4 cc = __ldg(reinterpret_cast<const int4 *>(g.tet_conn + 4 * (size_t)s));
-  nd[0] = cc.x; nd[1] = cc.y; nd[2] = cc.z; nd[3] = cc.w;
-  S T[4];
+__device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned char *stage, const TK<S> *sT,
+                                          const Curve<S> &kc, bool has_kf, int tid, uint16_t nd[4], S c[4]) {
+  const StageLayout<S> L(4, has_kf, g.tet_rank != nullptr);
+  const uint2 w = reinterpret_cast<const uint2 *>(stage + L.conn)[tid];
+  nd[0] = w.x & 0xffff; nd[1] = w.x >> 16; nd[2] = w.y & 0xffff; nd[3] = w.y >> 16;
+  S T[4], K[4];
 #pragma unroll
-  for (int b = 0; b < 4; ++b) T[b] = ldg(g.Tin + nd[b]);
-  const S *G = g.tet_G + 6 * (size_t)s;
-  const S g00 = ldg(G), g01 = ldg(G + 1), g02 = ldg(G + 2), g11 = ldg(G + 3), g12 = ldg(G + 4), g22 = ldg(G + 5);
-  S kb;
+  for (int b = 0; b < 4; ++b) {
+    const TK<S> q = sT[nd[b]];
+    T[b] = q.t;
+    K[b] = q.k;
+  }
+  const S *G = reinterpret_cast<const S *>(stage + L.G);
+  const S g00 = G[tid], g01 = G[kTileThreads + tid], g02 = G[2 * kTileThreads + tid],
+          g11 = G[3 * kTileThreads + tid], g12 = G[4 * kTileThreads + tid], g22 = G[5 * kTileThreads + tid];
+  const S kf = has_kf ? reinterpret_cast<const S *>(stage + L.kf)[tid] : S(1);
+  S kb = kf;
   if (TD) {
-    const Curve<S> &kc = g.mats.m[g.tet_region ? g.tet_region[s] : 0].k;
-    kb = kbar_of(g, kc, T, 4, g.tet_kf ? ldg(g.tet_kf + s) : S(1));
-  } else {
-    kb = ldg(g.tet_kf + s);
+    if (g.mats.n == 1) {  // k(T) staged per node: kbar = mean of the corner values
+      S sum = S(0);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) sum += K[b];
+      kb = sum / S(4) * kf;
+    } else {
+      kb = kbar_from(kc, T, 4, kf);
+    }
   }
   const S d1 = T[1] - T[0], d2 = T[2] - T[0], d3 = T[3] - T[0];
   c[1] = kb * (g00 * d1 + g01 * d2 + g02 * d3);
@@ -100,17 +233,25 @@ __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, int s, int32_t 
   c[0] = -((c[1] + c[2]) + c[3]);
 }
 
-// add -c[a] into the owned corners, one phase per barrier
-template <typename S, int N, bool UNIQ>
-__device__ __forceinline__ void accumulate(S *acc, const int32_t nd[N], const S c[N], int n0, int nfree,
-                                           bool valid, const uint8_t *rank, int n_phase) {
+// accumulation modes (deterministic in all three):
+//   kRanked      phase = rank of the slot among the node's slots of the batch
+//   kCornerPhase corner-unique tiles: phase = corner index (N barriers/batch)
+//   kCornerSlot  corner-unique tiles: one accumulator row per corner, plain
+//                stores, summed in corner order at the node update (1 barrier)
+enum { kRanked = 0, kCornerPhase = 1, kCornerSlot = 2 };
+
+template <typename S, int N, int MODE>
+__device__ __forceinline__ void accumulate(S *acc, const uint16_t nd[N], const S c[N], int nfree, bool valid,
+                                           const uint8_t *rank, int n_phase) {
   int loc[N];
 #pragma unroll
-  for (int a = 0; a < N; ++a) {
-    loc[a] = nd[a] - n0;
-    if (!valid || (unsigned)loc[a] >= (unsigned)nfree) loc[a] = -1;
-  }
-  if (UNIQ) {
+  for (int a = 0; a < N; ++a) loc[a] = (valid && nd[a] < nfree) ? (int)nd[a] : -1;
+  if (MODE == kCornerSlot) {
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+      if (loc[a] >= 0) acc[a * nfree + loc[a]] = -c[a];
+    __syncthreads();  // stage buffer fully consumed before it is refilled
+  } else if (MODE == kCornerPhase) {
 #pragma unroll
     for (int a = 0; a < N; ++a) {
       if (loc[a] >= 0) acc[loc[a]] -= c[a];
@@ -129,78 +270,116 @@ __device__ __forceinline__ void accumulate(S *acc, const int32_t nd[N], const S 
   }
 }
 
-template <typename S>
-__device__ __forceinline__ S sources_at(const TiledArgs<S> &g, const S *xyz) {
-  const S x = xyz[0], y = xyz[1], z = xyz[2];
-  S q = S(0);
-  for (int k = 0; k < g.n_src; ++k) {
-    const SourceT<S> &s = g.src[k];
-    if (!s.active) continue;
-    const S dx = x - s.cx, dy = y - s.cy, dz = z - s.cz;
-    const S r2 = (dx * dx + dy * dy) + dz * dz;
-    if (s.kind == FH_SOURCE_GAUSSIAN) {
-      q += s.amp * exp(-r2 * s.inv2s2);
-    } else {
-      q += r2 > S(0) ? min(s.cap, s.inv4pi_amp / r2) : s.cap;
-    }
-  }
-  return q;
-}
-
-template <typename S, bool TD, bool UNIQ>
+template <typename S, bool TD, int MODE>
 __global__ void __launch_bounds__(kTileThreads) k_tiled_step(const __grid_constant__ TiledArgs<S> g) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  S *acc = reinterpret_cast<S *>(smem_raw);
+  extern __shared__ __align__(128) unsigned char smem[];
+  TK<S> *sT = reinterpret_cast<TK<S> *>(smem);
+  S *acc = reinterpret_cast<S *>(smem + g.smem_T);
+  unsigned char *ring = smem + g.smem_T + g.smem_acc;
+  const int kStages = g.n_stages;
+  __shared__ __align__(8) uint64_t bars[kMaxStages];
   __shared__ int s_bad;
   if (g.flag->step != kNone) return;
   const int p = g.part_list ? g.part_list[g.part_begin + blockIdx.x] : g.part_begin + (int)blockIdx.x;
-  const int n0 = g.part_node_start[p];
-  const int nfree = g.part_n_free[p];
   const int tid = threadIdx.x;
-  if (tid == 0) s_bad = 0;
-  for (int i = tid; i < nfree; i += kTileThreads) acc[i] = S(0);
-  __syncthreads();
-
-  // tets
-  {
-    const int s0 = g.part_tet_start[p], s1 = g.part_tet_start[p + 1];
-    for (int b = s0; b < s1; b += kTileThreads) {
-      const int s = b + tid;
-      const bool valid = s < s1;
-      int32_t nd[4] = {0, 0, 0, 0};
-      S c[4] = {S(0), S(0), S(0), S(0)};
-      if (valid) tet_loads<S, TD>(g, s, nd, c);
-      uint8_t rk[4] = {0xff, 0xff, 0xff, 0xff};
-      if (!UNIQ && valid) {
-        const uint32_t w = __ldg(reinterpret_cast<const uint32_t *>(g.tet_rank) + s);
-        rk[0] = w & 0xff; rk[1] = (w >> 8) & 0xff; rk[2] = (w >> 16) & 0xff; rk[3] = w >> 24;
-      }
-      accumulate<S, 4, UNIQ>(acc, nd, c, n0, nfree, valid, rk, g.max_phase_tet);
+  const int n0 = g.part_node_start[p];
+  const int nn = g.part_node_start[p + 1] - n0;
+  const int nfree = g.part_n_free[p];
+  const int nbt = (g.part_tet_count[p] + kTileThreads - 1) / kTileThreads;
+  const int nbh = (g.part_hex_count[p] + kTileThreads - 1) / kTileThreads;
+  const int nb = nbt + nbh;
+  if (tid == 0) {
+    s_bad = 0;
+#pragma unroll
+    for (int q = 0; q < kStages; ++q) mbar_init(&bars[q], 1);
+    fence_barrier_init();
+    for (int j = 0; j < kStages && j < nb; ++j) issue_batch(g, p, j, nbt, ring + j * g.stage_bytes, &bars[j]);
+  }
+  // stage temperatures: owned range + halo list; zero accumulators
+  const bool kstage = TD && g.mats.n == 1;
+  const Curve<S> &k0 = g.mats.m[0].k;
+  constexpr int U = 4;  // loads in flight per thread while staging
+  for (int base = tid; base < nn; base += U * kTileThreads) {
+    S x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * kTileThreads;
+      x[u] = i < nn ? __ldg(g.Tin + n0 + i) : S(0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * kTileThreads;
+      if (i < nn) sT[i] = TK<S>{x[u], kstage ? interp(k0, x[u]) : S(0)};
     }
   }
-  // hexes
-  {
-    const int s0 = g.part_hex_start[p], s1 = g.part_hex_start[p + 1];
-    for (int b = s0; b < s1; b += kTileThreads) {
-      const int s = b + tid;
-      const bool valid = s < s1;
-      int32_t nd[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int h0 = g.part_halo_start[p], nh = g.part_halo_start[p + 1] - h0;
+  for (int base = tid; base < nh; base += U * kTileThreads) {
+    int id[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * kTileThreads;
+      id[u] = i < nh ? __ldg(g.halo_nodes + h0 + i) : 0;
+    }
+    S x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = __ldg(g.Tin + id[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * kTileThreads;
+      if (i < nh) sT[nn + i] = TK<S>{x[u], kstage ? interp(k0, x[u]) : S(0)};
+    }
+  }
+  for (int i = tid; i < (MODE == kCornerSlot ? 8 : 1) * nfree; i += kTileThreads) acc[i] = S(0);
+  __syncthreads();
+
+  for (int j = 0; j < nb; ++j) {
+    const int st = j % kStages;
+    unsigned char *stage = ring + st * g.stage_bytes;
+    mbar_wait(&bars[st], (uint32_t)((j / kStages) & 1));
+    const bool tet = j < nbt;
+    const int b = tet ? j : j - nbt;
+    const int cnt = tet ? g.part_tet_count[p] : g.part_hex_count[p];
+    const int slot = b * kTileThreads + tid;
+    const bool valid = slot < cnt;
+    if (tet) {
+      const int s = g.part_tet_start[p] + slot;
+      const Curve<S> &kc = g.mats.m[(g.tet_region && valid) ? g.tet_region[s] : 0].k;
+      uint16_t nd[4] = {0, 0, 0, 0};
+      S c[4] = {S(0), S(0), S(0), S(0)};
+      if (valid) tet_loads<S, TD>(g, stage, sT, kc, g.tet_kf != nullptr, tid, nd, c);
+      uint8_t rk[4] = {0xff, 0xff, 0xff, 0xff};
+      if (MODE == kRanked && valid) {
+        const StageLayout<S> L(4, g.tet_kf != nullptr, true);
+        const uint32_t w = reinterpret_cast<const uint32_t *>(stage + L.rank)[tid];
+        rk[0] = w & 0xff; rk[1] = (w >> 8) & 0xff; rk[2] = (w >> 16) & 0xff; rk[3] = w >> 24;
+      }
+      accumulate<S, 4, MODE>(acc, nd, c, nfree, valid, rk, g.max_phase_tet);
+    } else {
+      const int s = g.part_hex_start[p] + slot;
+      const Curve<S> &kc = g.mats.m[(g.hex_region && valid) ? g.hex_region[s] : 0].k;
+      uint16_t nd[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       S c[8];
 #pragma unroll
       for (int a = 0; a < 8; ++a) c[a] = S(0);
-      if (valid) hex_loads<S, TD>(g, s, nd, c);
+      if (valid) hex_loads<S, TD>(g, stage, sT, kc, g.hex_kf != nullptr, tid, nd, c);
       uint8_t rk[8];
 #pragma unroll
       for (int a = 0; a < 8; ++a) rk[a] = 0xff;
-      if (!UNIQ && valid) {
-        const uint2 w = __ldg(reinterpret_cast<const uint2 *>(g.hex_rank) + s);
+      if (MODE == kRanked && valid) {
+        const StageLayout<S> L(8, g.hex_kf != nullptr, true);
+        const uint2 w = reinterpret_cast<const uint2 *>(stage + L.rank)[tid];
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
           rk[a] = (w.x >> (8 * a)) & 0xff;
           rk[a + 4] = (w.y >> (8 * a)) & 0xff;
         }
       }
-      accumulate<S, 8, UNIQ>(acc, nd, c, n0, nfree, valid, rk, g.max_phase_hex);
+      accumulate<S, 8, MODE>(acc, nd, c, nfree, valid, rk, g.max_phase_hex);
+    }
+    // every thread passed the last phase barrier: the stage can be refilled
+    if (tid == 0 && j + kStages < nb) {
+      fence_proxy_async();
+      issue_batch(g, p, j + kStages, nbt, stage, &bars[st]);
     }
   }
   __syncthreads();
@@ -208,29 +387,56 @@ __global__ void __launch_bounds__(kTileThreads) k_tiled_step(const __grid_consta
   // lumped nodal update of the owned free nodes
   bool bad = false;
   const int rstart = g.part_robin_start[p];
-  for (int loc = tid; loc < nfree; loc += kTileThreads) {
-    const int n = n0 + loc;
-    const S x = g.Tin[n];
-    const S v = g.vol[n];
-    const Mat<S> &m = g.mats.m[g.node_region ? g.node_region[n] : 0];
-    S cap, kb;
-    if (TD) {
-      cap = interp(m.rho, x) * interp(m.c, x) * v;
-      kb = m.td_perf ? interp(m.wb, x) * m.cb * v : m.wbcb * v;
-    } else {
-      cap = g.cap_frozen[n];
-      kb = m.td_perf ? g.kb_frozen[n] : m.wbcb * v;
+  constexpr int UN = 4;  // nodes per thread per round: their global loads are issued together
+  for (int base = tid; base < nfree; base += UN * kTileThreads) {
+    S v[UN], q[UN], cf[UN], kf[UN], px[UN], py[UN], pz[UN];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int loc = base + u * kTileThreads;
+      const bool ok = loc < nfree;
+      const int n = n0 + (ok ? loc : 0);
+      v[u] = __ldg(g.vol + n);
+      q[u] = g.q_ext ? __ldg(g.q_ext + n) : S(0);
+      cf[u] = TD ? S(0) : __ldg(g.cap_frozen + n);
+      kf[u] = (!TD && g.kb_frozen) ? __ldg(g.kb_frozen + n) : S(0);
+      if (g.n_src) {
+        px[u] = __ldg(g.xyz + 3 * (size_t)n);
+        py[u] = __ldg(g.xyz + 3 * (size_t)n + 1);
+        pz[u] = __ldg(g.xyz + 3 * (size_t)n + 2);
+      }
     }
-    S rate = ((acc[loc] - mul_rn(kb, x)) + mul_rn(kb, m.Ta)) + m.Qm * v;
-    if (g.q_ext) rate += g.q_ext[n];
-    if (g.n_src) rate += sources_at(g, g.xyz + 3 * (size_t)n) * v;
-    if (loc >= rstart) {
-      const int rb = g.part_robin_base[p] + (loc - rstart);
-      rate += g.robin_hAT[rb] - g.robin_hA[rb] * x;
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int loc = base + u * kTileThreads;
+      if (loc >= nfree) continue;
+      const int n = n0 + loc;
+      const S x = sT[loc].t;
+      S Fsum;
+      if (MODE == kCornerSlot) {  // corner slots summed in fixed corner order: deterministic
+        Fsum = ((acc[loc] + acc[nfree + loc]) + (acc[2 * nfree + loc] + acc[3 * nfree + loc])) +
+               ((acc[4 * nfree + loc] + acc[5 * nfree + loc]) + (acc[6 * nfree + loc] + acc[7 * nfree + loc]));
+      } else {
+        Fsum = acc[loc];
+      }
+      S rate;
+      S cap;
+      // single material: curve parameters are uniform kernel-parameter operands
+      if (!g.node_region)
+        rate = node_rate<S, TD>(g.mats.m[0], x, Fsum, v[u], q[u], cf[u], kf[u], cap);
+      else
+        rate = node_rate<S, TD>(g.mats.m[g.node_region[n]], x, Fsum, v[u], q[u], cf[u], kf[u], cap);
+      if (g.n_src) {
+        const S xyz[3] = {px[u], py[u], pz[u]};
+        rate += sources_at(g, xyz) * v[u];
+      }
+      if (loc >= rstart) {
+        const int rb = g.part_robin_base[p] + (loc - rstart);
+        rate += g.robin_hAT[rb] - g.robin_hA[rb] * x;
+      }
+      const S xn = x + fast_div(g.dt * rate, cap);
+      g.Tout[n] = xn;
+      bad |= !(fabs(xn) <= g.runaway_limit);  // also catches NaN
     }
-    const S xn = x + g.dt * rate / cap;
-    g.Tout[n] = xn;
-    bad |= !(fabs(xn) <= g.runaway_limit);  // also catches NaN
   }
   if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) s_bad = 1;
   __syncthreads();
@@ -238,12 +444,16 @@ __global__ void __launch_bounds__(kTileThreads) k_tiled_step(const __grid_consta
 }
 
 template <typename S>
-static void launch_step(const TiledArgs<S> &g, int n_parts, bool td, bool uniq, size_t smem, cudaStream_t s) {
+void tiled_step(const TiledArgs<S> &g, int n_parts, bool td, int mode_sel, size_t smem, cudaStream_t s) {
   if (n_parts <= 0) return;
-  auto kern = td ? (uniq ? k_tiled_step<S, true, true> : k_tiled_step<S, true, false>)
-                 : (uniq ? k_tiled_step<S, false, true> : k_tiled_step<S, false, false>);
-  static size_t configured[2][2] = {{0, 0}, {0, 0}};
-  size_t &cfg = configured[td][uniq];
+  using K = void (*)(TiledArgs<S>);
+  static const K table[2][3] = {
+      {k_tiled_step<S, false, kRanked>, k_tiled_step<S, false, kCornerPhase>, k_tiled_step<S, false, kCornerSlot>},
+      {k_tiled_step<S, true, kRanked>, k_tiled_step<S, true, kCornerPhase>, k_tiled_step<S, true, kCornerSlot>}};
+  const int mode = mode_sel < 0 || mode_sel > 2 ? 0 : mode_sel;
+  const K kern = table[td ? 1 : 0][mode];
+  static size_t configured[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  size_t &cfg = configured[td ? 1 : 0][mode];
   if (smem > cfg) {
     FH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cfg = smem;
@@ -251,13 +461,8 @@ static void launch_step(const TiledArgs<S> &g, int n_parts, bool td, bool uniq, 
   kern<<<n_parts, kTileThreads, smem, s>>>(g);
   FH_CUDA(cudaGetLastError());
 }
-
-void tiled_step(const TiledArgs<float> &g, int n_parts, bool td, bool uniq, size_t smem, cudaStream_t s) {
-  launch_step(g, n_parts, td, uniq, smem, s);
-}
-void tiled_step(const TiledArgs<double> &g, int n_parts, bool td, bool uniq, size_t smem, cudaStream_t s) {
-  launch_step(g, n_parts, td, uniq, smem, s);
-}
+template void tiled_step<float>(const TiledArgs<float> &, int, bool, int, size_t, cudaStream_t);
+template void tiled_step<double>(const TiledArgs<double> &, int, bool, int, size_t, cudaStream_t);
 
 // ---- TI freeze ---------------------------------------------------------------
 template <typename S, int N>
@@ -269,7 +474,7 @@ __global__ void k_freeze_slots(const TiledArgs<S> g, const int32_t *__restrict__
   S T[8];
 #pragma unroll
   for (int b = 0; b < 8; ++b) T[b] = b < N ? g.Tin[conn[N * s + b]] : S(0);
-  kbar[s] = kbar_of(g, kc, T, N, kf ? kf[s] : S(1));
+  kbar[s] = kbar_from(kc, T, N, kf ? kf[s] : S(1));
 }
 
 template <typename S>
@@ -283,18 +488,20 @@ __global__ void k_freeze_nodes(const TiledArgs<S> g, int64_t V, S *__restrict__ 
 }
 
 template <typename S>
-void tiled_freeze(const TiledArgs<S> &g, int64_t nt, int64_t nh, int64_t V, const S *kf_tet, const S *kf_hex,
-                  S *kbar_tet, S *kbar_hex, S *cap, S *kb, cudaStream_t s) {
-  if (nt) k_freeze_slots<S, 4><<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(g, g.tet_conn, g.tet_region, nt, kf_tet, kbar_tet);
-  if (nh) k_freeze_slots<S, 8><<<(unsigned)((nh + 255) / 256), 256, 0, s>>>(g, g.hex_conn, g.hex_region, nh, kf_hex, kbar_hex);
+void tiled_freeze(const TiledArgs<S> &g, const int32_t *tet_conn, const int32_t *hex_conn, int64_t nt, int64_t nh,
+                  int64_t V, const S *kf_tet, const S *kf_hex, S *kbar_tet, S *kbar_hex, S *cap, S *kb,
+                  cudaStream_t s) {
+  if (nt) k_freeze_slots<S, 4><<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(g, tet_conn, g.tet_region, nt, kf_tet, kbar_tet);
+  if (nh) k_freeze_slots<S, 8><<<(unsigned)((nh + 255) / 256), 256, 0, s>>>(g, hex_conn, g.hex_region, nh, kf_hex, kbar_hex);
   if (V) k_freeze_nodes<S><<<(unsigned)((V + 255) / 256), 256, 0, s>>>(g, V, cap, kb);
   FH_CUDA(cudaGetLastError());
 }
-
-template void tiled_freeze<float>(const TiledArgs<float> &, int64_t, int64_t, int64_t, const float *, const float *,
-                                  float *, float *, float *, float *, cudaStream_t);
-template void tiled_freeze<double>(const TiledArgs<double> &, int64_t, int64_t, int64_t, const double *,
-                                   const double *, double *, double *, double *, double *, cudaStream_t);
+template void tiled_freeze<float>(const TiledArgs<float> &, const int32_t *, const int32_t *, int64_t, int64_t,
+                                  int64_t, const float *, const float *, float *, float *, float *, float *,
+                                  cudaStream_t);
+template void tiled_freeze<double>(const TiledArgs<double> &, const int32_t *, const int32_t *, int64_t, int64_t,
+                                   int64_t, const double *, const double *, double *, double *, double *, double *,
+                                   cudaStream_t);
 
 template <typename S>
 __global__ void k_probes_t(const S *__restrict__ T, const int32_t *__restrict__ probes, int64_t np,

@@ -4,7 +4,8 @@
 
 namespace fh {
 
-constexpr int kTileThreads = 256;  // == partition batch size
+constexpr int kTileThreads = 256;  // == partition batch size B
+constexpr int kMaxStages = 4;      // TMA ring depth limit (batches in flight per CTA)
 
 template <typename S>
 struct SourceT {
@@ -14,20 +15,27 @@ struct SourceT {
   int active;
 };
 
+// Slot streams of a part are stored in batches of kTileThreads slots, every
+// part's range starting on a batch boundary:
+//   conn16 [slot][N]   uint16 tile-local node index (owned | halo)
+//   G      [batch][6][B] metric tensor components (hex pre-scaled by 1/64)
+//   kf     [slot]      conductivity factor (TD) or frozen kbar (TI), optional
+//   rank   [slot][N]   accumulation phase per corner (ranked mode only)
 template <typename S>
 struct TiledArgs {
-  // part tables
   const int32_t *part_list;  // parts processed by this launch: part_list[part_begin + blockIdx.x]
   int32_t part_begin;
   const int32_t *part_node_start, *part_n_free, *part_robin_start, *part_robin_base;
-  const int32_t *part_tet_start, *part_hex_start;
-  // slots
-  const int32_t *tet_conn, *hex_conn;   // new node ids, 4 / 8 per slot
-  const S *tet_G, *hex_G;               // 6 per slot (hex pre-scaled by 1/64)
-  const S *tet_kf, *hex_kf;             // per-slot conductivity factor, or frozen kbar (TI), or null
-  const uint8_t *tet_rank, *hex_rank;   // phases (ranked mode) or null (corner-unique)
+  const int32_t *part_tet_start, *part_tet_count, *part_hex_start, *part_hex_count;
+  const int32_t *part_halo_start, *halo_nodes;
+  const uint16_t *tet_conn16, *hex_conn16;
+  const S *tet_G, *hex_G;
+  const S *tet_kf, *hex_kf;
+  const uint8_t *tet_rank, *hex_rank;  // null: corner-unique (phase == corner)
   const uint8_t *tet_region, *hex_region;
   int max_phase_tet, max_phase_hex;
+  // smem carve-up (bytes) and ring depth
+  int smem_T, smem_acc, stage_bytes, n_stages;
   // nodes (new numbering)
   const S *Tin;
   S *Tout;
@@ -41,21 +49,32 @@ struct TiledArgs {
   int n_src;
   SourceT<S> src[kMaxSources];
   S dt, runaway_limit;
-  int frozen_kbar;  // TI: *_kf hold kbar
   FailFlag *flag;
   unsigned long long step_no;
 };
 
-void tiled_step(const TiledArgs<float> &g, int n_parts, bool td, bool corner_unique, size_t smem,
-                cudaStream_t s);
-void tiled_step(const TiledArgs<double> &g, int n_parts, bool td, bool corner_unique, size_t smem,
-                cudaStream_t s);
-
-// TI freeze: per-slot kbar (into kbar_tet / kbar_hex, using the factor
-// arrays kf_tet / kf_hex if given) and per-node capacity / perfusion from Tin.
+// bytes of one staged batch: conn16 [B][N] | G [6][B] | kf [B] | rank [B][N]
 template <typename S>
-void tiled_freeze(const TiledArgs<S> &g, int64_t n_tet_slots, int64_t n_hex_slots, int64_t n_nodes,
-                  const S *kf_tet, const S *kf_hex, S *kbar_tet, S *kbar_hex, S *cap, S *kb, cudaStream_t s);
+inline int StageBytes(int N, bool has_kf, bool has_rank) {
+  int b = kTileThreads * N * 2 + 6 * kTileThreads * (int)sizeof(S);
+  if (has_kf) b += kTileThreads * (int)sizeof(S);
+  if (has_rank) b += kTileThreads * N;
+  return (b + 15) & ~15;
+}
+
+template <typename S>
+void tiled_step(const TiledArgs<S> &g, int n_parts, bool td, int mode, size_t smem, cudaStream_t s);
+
+// accumulation mode of the step kernel (see fh_tiled.cu): 0 ranked phases,
+// 1 corner phases, 2 corner slots (the last two need corner-unique tiles)
+enum TileMode { kModeRanked = 0, kModeCornerPhase = 1, kModeCornerSlot = 2 };
+
+// TI freeze: per-slot kbar (global-id connectivity conn4/conn8) and per-node
+// capacity / perfusion from Tin.
+template <typename S>
+void tiled_freeze(const TiledArgs<S> &g, const int32_t *tet_conn, const int32_t *hex_conn, int64_t n_tet_slots,
+                  int64_t n_hex_slots, int64_t n_nodes, const S *kf_tet, const S *kf_hex, S *kbar_tet,
+                  S *kbar_hex, S *cap, S *kb, cudaStream_t s);
 
 template <typename S>
 void gather_probes_t(const S *T, const int32_t *probes, int64_t np, double *out, const FailFlag *flag,

@@ -1,0 +1,52 @@
+"""Tuning sweep of the fused step on one workload (GPU): tile size x
+accumulation mode x TMA ring depth.  The mesh is built once; each variant
+gets its own engine.  Prints one line per variant."""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1909_05098_b200 as fh  # noqa: E402
+from paper_1909_05098_b200 import _native as N  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg4")
+ap.add_argument("--divisions", type=int, default=0)
+ap.add_argument("--precision", type=int, default=0)
+ap.add_argument("--parts", default="768,1024")
+ap.add_argument("--modes", default="1,2")
+ap.add_argument("--stages", default="2,3")
+ap.add_argument("--steps", type=int, default=50)
+args = ap.parse_args()
+
+prob = bench.make_problem(args.config, args.divisions, args.precision)
+peak, _ = bench.peaks()
+t0 = time.time()
+for pn in [int(x) for x in args.parts.split(",")]:
+    for mode in [int(x) for x in args.modes.split(",")]:
+        for stg in [int(x) for x in args.stages.split(",")]:
+            os.environ["FH_TILE_MODE"] = str(mode)
+            os.environ["FH_TILE_STAGES"] = str(stg)
+            eng = fh.ExplicitEngine(prob.mesh, prob.material, prob.boundary, assembly="tiled", part_nodes=pn,
+                                    **prob.engine_kwargs())
+            dt = 0.9 * eng.critical_dt(37.0)
+            st = eng.initial_state(37.0)
+            L, h = eng._L, eng._h
+            N.check(L.fh_set_temperature(h, N.ptr(st.temperatures), st.temperatures.size, 0, 0.0))
+            rep = N.FhReport()
+            el = C.c_float()
+            N.check(L.fh_step_timed(h, 5, dt, C.byref(rep), C.byref(el)))
+            N.check(L.fh_step_timed(h, args.steps, dt, C.byref(rep), C.byref(el)))
+            ms = el.value / args.steps
+            lay = eng.layout()
+            frac = lay["canonical_bytes"] / (ms / 1e3) / 1e9 / peak
+            print(json.dumps({"part_nodes": pn, "mode": mode, "stages": stg, "ms": round(ms, 4),
+                              "frac": round(frac, 4), "parts": lay["n_parts"], "slots": lay["n_slots"]}), flush=True)
+            del eng
+print("sweep wall", time.time() - t0)

@@ -109,9 +109,9 @@ __global__ void k_pack_slots(const int32_t *__restrict__ slot_elem, int64_t n, c
   if (s >= n) return;
   const int64_t e = slot_elem[s];
   // G in batch-major SoA: [s / B][component][s % B]
-  const int64_t base = (s / kTileThreads) * 6 * kTileThreads + (s % kTileThreads);
+  const int64_t base = (s / kBatch) * 6 * kBatch + (s % kBatch);
 #pragma unroll
-  for (int k = 0; k < 6; ++k) out_G[base + k * kTileThreads] = e >= 0 ? (S)(G[6 * e + k] * scale) : S(0);
+  for (int k = 0; k < 6; ++k) out_G[base + k * kBatch] = e >= 0 ? (S)(G[6 * e + k] * scale) : S(0);
   if (out_kf) out_kf[s] = e >= 0 ? (S)kf[e] : S(1);
   if (out_region) out_region[s] = e >= 0 ? (uint8_t)region[e] : 0;
 }
@@ -352,8 +352,8 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   pin.tets = mesh.tets;
   pin.hexes = mesh.hexes;
   pin.node_class = cls.data();
-  pin.target_part_nodes = o.part_nodes > 0 ? o.part_nodes : (sizeof(S) == 4 ? 2048 : 1024);
-  pin.batch = kTileThreads;
+  pin.target_part_nodes = o.part_nodes > 0 ? o.part_nodes : (sizeof(S) == 4 ? 1536 : 768);
+  pin.batch = kBatch;
   pin.n_domains = std::max(1, o.n_domains);
   pin.slab_axis = o.slab_axis;
   build_partition(pin, e->part);
@@ -511,7 +511,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     const int m = atoi(env);
     if (m == kModeRanked || P.corner_unique) st->mode = m;
   }
-  g.n_stages = 3;
+  g.n_stages = 2;  // measured best on cfg4 (scripts/sweep.py)
   if (const char *env = getenv("FH_TILE_STAGES")) g.n_stages = std::min(kMaxStages, std::max(1, atoi(env)));
   g.smem_T = (int)al(2 * sizeof(S) * (size_t)std::max(1, P.max_local_nodes));
   g.smem_acc = (int)al(sizeof(S) * (st->mode == kModeCornerSlot ? 8 : 1) * (size_t)std::max(1, P.max_part_free));

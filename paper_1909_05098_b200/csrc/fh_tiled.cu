@@ -73,10 +73,10 @@ struct StageLayout {
   int conn, G, kf, rank, bytes;
   __host__ __device__ StageLayout(int N, bool has_kf, bool has_rank) {
     conn = 0;
-    G = kTileThreads * N * 2;
-    kf = G + 6 * kTileThreads * (int)sizeof(S);
-    rank = kf + (has_kf ? kTileThreads * (int)sizeof(S) : 0);
-    bytes = rank + (has_rank ? kTileThreads * N : 0);
+    G = kBatch * N * 2;
+    kf = G + 6 * kBatch * (int)sizeof(S);
+    rank = kf + (has_kf ? kBatch * (int)sizeof(S) : 0);
+    bytes = rank + (has_rank ? kBatch * N : 0);
     bytes = (bytes + 15) & ~15;
   }
 };
@@ -131,9 +131,9 @@ __device__ void issue_batch(const TiledArgs<S> &g, int p, int j, int nbt, unsign
   const bool tet = j < nbt;
   const int N = tet ? 4 : 8;
   const int b = tet ? j : j - nbt;
-  const int s0 = (tet ? g.part_tet_start[p] : g.part_hex_start[p]) + b * kTileThreads;
-  const int cnt = (tet ? g.part_tet_count[p] : g.part_hex_count[p]) - b * kTileThreads;
-  const int k = cnt < kTileThreads ? cnt : kTileThreads;
+  const int s0 = (tet ? g.part_tet_start[p] : g.part_hex_start[p]) + b * kBatch;
+  const int cnt = (tet ? g.part_tet_count[p] : g.part_hex_count[p]) - b * kBatch;
+  const int k = cnt < kBatch ? cnt : kBatch;
   const int kr = (k + 3) & ~3;
   const uint16_t *conn = tet ? g.tet_conn16 : g.hex_conn16;
   const S *G = tet ? g.tet_G : g.hex_G;
@@ -145,20 +145,20 @@ __device__ void issue_batch(const TiledArgs<S> &g, int p, int j, int nbt, unsign
   if (rank) bytes += kr * N;
   mbar_expect_tx(bar, bytes);
   bulk_g2s(stage + L.conn, conn + (size_t)N * s0, kr * N * 2, bar);
-  const S *Gb = G + (size_t)(s0 / kTileThreads) * 6 * kTileThreads;
+  const S *Gb = G + (size_t)(s0 / kBatch) * 6 * kBatch;
 #pragma unroll
   for (int c = 0; c < 6; ++c)
-    bulk_g2s(stage + L.G + c * kTileThreads * sizeof(S), Gb + c * kTileThreads, kr * sizeof(S), bar);
+    bulk_g2s(stage + L.G + c * kBatch * sizeof(S), Gb + c * kBatch, kr * sizeof(S), bar);
   if (kf) bulk_g2s(stage + L.kf, kf + s0, kr * sizeof(S), bar);
   if (rank) bulk_g2s(stage + L.rank, rank + (size_t)N * s0, kr * N, bar);
 }
 
-// element loads from the staged batch -----------------------------------------
+// element loads of staged slot i of the batch ------------------------------------
 template <typename S, bool TD>
 __device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned char *stage, const TK<S> *sT,
-                                          const Curve<S> &kc, bool has_kf, int tid, uint16_t nd[8], S c[8]) {
+                                          const Curve<S> &kc, bool has_kf, int i, uint16_t nd[8], S c[8]) {
   const StageLayout<S> L(8, has_kf, g.hex_rank != nullptr);
-  const uint4 w = reinterpret_cast<const uint4 *>(stage + L.conn)[tid];
+  const uint4 w = reinterpret_cast<const uint4 *>(stage + L.conn)[i];
   nd[0] = w.x & 0xffff; nd[1] = w.x >> 16; nd[2] = w.y & 0xffff; nd[3] = w.y >> 16;
   nd[4] = w.z & 0xffff; nd[5] = w.z >> 16; nd[6] = w.w & 0xffff; nd[7] = w.w >> 16;
   S T[8], K[8];
@@ -169,27 +169,23 @@ __device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned 
     K[b] = q.k;
   }
   const S *G = reinterpret_cast<const S *>(stage + L.G);
-  const S g00 = G[tid], g01 = G[kTileThreads + tid], g02 = G[2 * kTileThreads + tid],
-          g11 = G[3 * kTileThreads + tid], g12 = G[4 * kTileThreads + tid], g22 = G[5 * kTileThreads + tid];
-  const S kf = has_kf ? reinterpret_cast<const S *>(stage + L.kf)[tid] : S(1);
+  const S g00 = G[i], g01 = G[kBatch + i], g02 = G[2 * kBatch + i], g11 = G[3 * kBatch + i],
+          g12 = G[4 * kBatch + i], g22 = G[5 * kBatch + i];
+  const S kf = has_kf ? reinterpret_cast<const S *>(stage + L.kf)[i] : S(1);
   S kb = kf;
   if (TD) {
     if (g.mats.n == 1) {  // k(T) staged per node: kbar = mean of the corner values
-      S sum = S(0);
-#pragma unroll
-      for (int b = 0; b < 8; ++b) sum += K[b];
-      kb = sum / S(8) * kf;
+      const S sum = ((K[0] + K[1]) + (K[2] + K[3])) + ((K[4] + K[5]) + (K[6] + K[7]));
+      kb = sum * S(0.125) * kf;
     } else {
       kb = kbar_from(kc, T, 8, kf);
     }
   }
-  S d[8];
-#pragma unroll
-  for (int b = 0; b < 8; ++b) d[b] = T[b] - T[0];
-  // g = sum_b s_b d_b with the corner signs of element.py HEX_VERTEX_SIGNS
-  const S gx = ((d[1] - d[0]) + (d[2] - d[3])) + ((d[5] - d[4]) + (d[6] - d[7]));
-  const S gy = ((d[3] - d[0]) + (d[2] - d[1])) + ((d[7] - d[4]) + (d[6] - d[5]));
-  const S gz = ((d[4] - d[0]) + (d[5] - d[1])) + ((d[6] - d[2]) + (d[7] - d[3]));
+  // g = sum_b s_b (T_b - T_0) with the corner signs of element.py HEX_VERTEX_SIGNS
+  // (the T_0 shifts cancel pairwise except where written explicitly)
+  const S gx = ((T[1] - T[0]) + (T[2] - T[3])) + ((T[5] - T[4]) + (T[6] - T[7]));
+  const S gy = ((T[3] - T[0]) + (T[2] - T[1])) + ((T[7] - T[4]) + (T[6] - T[5]));
+  const S gz = ((T[4] - T[0]) + (T[5] - T[1])) + ((T[6] - T[2]) + (T[7] - T[3]));
   const S u = kb * (g00 * gx + g01 * gy + g02 * gz);
   const S v = kb * (g01 * gx + g11 * gy + g12 * gz);
   const S w2 = kb * (g02 * gx + g12 * gy + g22 * gz);
@@ -200,9 +196,9 @@ __device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned 
 
 template <typename S, bool TD>
 __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned char *stage, const TK<S> *sT,
-                                          const Curve<S> &kc, bool has_kf, int tid, uint16_t nd[4], S c[4]) {
+                                          const Curve<S> &kc, bool has_kf, int i, uint16_t nd[4], S c[4]) {
   const StageLayout<S> L(4, has_kf, g.tet_rank != nullptr);
-  const uint2 w = reinterpret_cast<const uint2 *>(stage + L.conn)[tid];
+  const uint2 w = reinterpret_cast<const uint2 *>(stage + L.conn)[i];
   nd[0] = w.x & 0xffff; nd[1] = w.x >> 16; nd[2] = w.y & 0xffff; nd[3] = w.y >> 16;
   S T[4], K[4];
 #pragma unroll
@@ -212,16 +208,13 @@ __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned 
     K[b] = q.k;
   }
   const S *G = reinterpret_cast<const S *>(stage + L.G);
-  const S g00 = G[tid], g01 = G[kTileThreads + tid], g02 = G[2 * kTileThreads + tid],
-          g11 = G[3 * kTileThreads + tid], g12 = G[4 * kTileThreads + tid], g22 = G[5 * kTileThreads + tid];
-  const S kf = has_kf ? reinterpret_cast<const S *>(stage + L.kf)[tid] : S(1);
+  const S g00 = G[i], g01 = G[kBatch + i], g02 = G[2 * kBatch + i], g11 = G[3 * kBatch + i],
+          g12 = G[4 * kBatch + i], g22 = G[5 * kBatch + i];
+  const S kf = has_kf ? reinterpret_cast<const S *>(stage + L.kf)[i] : S(1);
   S kb = kf;
   if (TD) {
-    if (g.mats.n == 1) {  // k(T) staged per node: kbar = mean of the corner values
-      S sum = S(0);
-#pragma unroll
-      for (int b = 0; b < 4; ++b) sum += K[b];
-      kb = sum / S(4) * kf;
+    if (g.mats.n == 1) {
+      kb = ((K[0] + K[1]) + (K[2] + K[3])) * S(0.25) * kf;
     } else {
       kb = kbar_from(kc, T, 4, kf);
     }
@@ -238,38 +231,43 @@ __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned 
 //   kCornerPhase corner-unique tiles: phase = corner index (N barriers/batch)
 //   kCornerSlot  corner-unique tiles: one accumulator row per corner, plain
 //                stores, summed in corner order at the node update (1 barrier)
+// Each thread carries kSPT slots of the batch (i = q * kTileThreads + tid).
 enum { kRanked = 0, kCornerPhase = 1, kCornerSlot = 2 };
 
 template <typename S, int N, int MODE>
-__device__ __forceinline__ void accumulate(S *acc, const uint16_t nd[N], const S c[N], int nfree, bool valid,
-                                           const uint8_t *rank, int n_phase) {
-  int loc[N];
+__device__ __forceinline__ void accumulate(S *acc, const uint16_t (&nd)[kSPT][N], const S (&c)[kSPT][N], int nfree,
+                                           const bool (&valid)[kSPT], const uint8_t (&rank)[kSPT][N], int n_phase) {
+  int loc[kSPT][N];
 #pragma unroll
-  for (int a = 0; a < N; ++a) loc[a] = (valid && nd[a] < nfree) ? (int)nd[a] : -1;
+  for (int q = 0; q < kSPT; ++q)
+#pragma unroll
+    for (int a = 0; a < N; ++a) loc[q][a] = (valid[q] && nd[q][a] < nfree) ? (int)nd[q][a] : -1;
   if (MODE == kCornerSlot) {
 #pragma unroll
-    for (int a = 0; a < N; ++a)
-      if (loc[a] >= 0) acc[a * nfree + loc[a]] = -c[a];
+    for (int q = 0; q < kSPT; ++q)
+#pragma unroll
+      for (int a = 0; a < N; ++a)
+        if (loc[q][a] >= 0) acc[a * nfree + loc[q][a]] = -c[q][a];
     __syncthreads();  // stage buffer fully consumed before it is refilled
   } else if (MODE == kCornerPhase) {
 #pragma unroll
     for (int a = 0; a < N; ++a) {
-      if (loc[a] >= 0) acc[loc[a]] -= c[a];
+#pragma unroll
+      for (int q = 0; q < kSPT; ++q)
+        if (loc[q][a] >= 0) acc[loc[q][a]] -= c[q][a];
       __syncthreads();
     }
   } else {
-    uint8_t r[N];
-#pragma unroll
-    for (int a = 0; a < N; ++a) r[a] = valid ? rank[a] : 0xff;
     for (int ph = 0; ph < n_phase; ++ph) {
 #pragma unroll
-      for (int a = 0; a < N; ++a)
-        if (r[a] == ph && loc[a] >= 0) acc[loc[a]] -= c[a];
+      for (int q = 0; q < kSPT; ++q)
+#pragma unroll
+        for (int a = 0; a < N; ++a)
+          if (rank[q][a] == ph && loc[q][a] >= 0) acc[loc[q][a]] -= c[q][a];
       __syncthreads();
     }
   }
 }
-
 template <typename S, bool TD, int MODE>
 __global__ void __launch_bounds__(kTileThreads) k_tiled_step(const __grid_constant__ TiledArgs<S> g) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -285,8 +283,8 @@ __global__ void __launch_bounds__(kTileThreads) k_tiled_step(const __grid_consta
   const int n0 = g.part_node_start[p];
   const int nn = g.part_node_start[p + 1] - n0;
   const int nfree = g.part_n_free[p];
-  const int nbt = (g.part_tet_count[p] + kTileThreads - 1) / kTileThreads;
-  const int nbh = (g.part_hex_count[p] + kTileThreads - 1) / kTileThreads;
+  const int nbt = (g.part_tet_count[p] + kBatch - 1) / kBatch;
+  const int nbh = (g.part_hex_count[p] + kBatch - 1) / kBatch;
   const int nb = nbt + nbh;
   if (tid == 0) {
     s_bad = 0;
@@ -332,46 +330,64 @@ __global__ void __launch_bounds__(kTileThreads) k_tiled_step(const __grid_consta
   for (int i = tid; i < (MODE == kCornerSlot ? 8 : 1) * nfree; i += kTileThreads) acc[i] = S(0);
   __syncthreads();
 
+  int st = 0;
+  uint32_t parity = 0;
   for (int j = 0; j < nb; ++j) {
-    const int st = j % kStages;
     unsigned char *stage = ring + st * g.stage_bytes;
-    mbar_wait(&bars[st], (uint32_t)((j / kStages) & 1));
+    mbar_wait(&bars[st], parity);
     const bool tet = j < nbt;
     const int b = tet ? j : j - nbt;
     const int cnt = tet ? g.part_tet_count[p] : g.part_hex_count[p];
-    const int slot = b * kTileThreads + tid;
-    const bool valid = slot < cnt;
+    bool valid[kSPT];
+#pragma unroll
+    for (int q = 0; q < kSPT; ++q) valid[q] = b * kBatch + q * kTileThreads + tid < cnt;
     if (tet) {
-      const int s = g.part_tet_start[p] + slot;
-      const Curve<S> &kc = g.mats.m[(g.tet_region && valid) ? g.tet_region[s] : 0].k;
-      uint16_t nd[4] = {0, 0, 0, 0};
-      S c[4] = {S(0), S(0), S(0), S(0)};
-      if (valid) tet_loads<S, TD>(g, stage, sT, kc, g.tet_kf != nullptr, tid, nd, c);
-      uint8_t rk[4] = {0xff, 0xff, 0xff, 0xff};
-      if (MODE == kRanked && valid) {
-        const StageLayout<S> L(4, g.tet_kf != nullptr, true);
-        const uint32_t w = reinterpret_cast<const uint32_t *>(stage + L.rank)[tid];
-        rk[0] = w & 0xff; rk[1] = (w >> 8) & 0xff; rk[2] = (w >> 16) & 0xff; rk[3] = w >> 24;
+      uint16_t nd[kSPT][4];
+      S c[kSPT][4];
+      uint8_t rk[kSPT][4];
+#pragma unroll
+      for (int q = 0; q < kSPT; ++q) {
+        const int i = q * kTileThreads + tid;
+        const int s = g.part_tet_start[p] + b * kBatch + i;
+        const Curve<S> &kc = g.mats.m[(g.tet_region && valid[q]) ? g.tet_region[s] : 0].k;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          nd[q][a] = 0;
+          c[q][a] = S(0);
+          rk[q][a] = 0xff;
+        }
+        if (valid[q]) tet_loads<S, TD>(g, stage, sT, kc, g.tet_kf != nullptr, i, nd[q], c[q]);
+        if (MODE == kRanked && valid[q]) {
+          const StageLayout<S> L(4, g.tet_kf != nullptr, true);
+          const uint32_t w = reinterpret_cast<const uint32_t *>(stage + L.rank)[i];
+          rk[q][0] = w & 0xff; rk[q][1] = (w >> 8) & 0xff; rk[q][2] = (w >> 16) & 0xff; rk[q][3] = w >> 24;
+        }
       }
       accumulate<S, 4, MODE>(acc, nd, c, nfree, valid, rk, g.max_phase_tet);
     } else {
-      const int s = g.part_hex_start[p] + slot;
-      const Curve<S> &kc = g.mats.m[(g.hex_region && valid) ? g.hex_region[s] : 0].k;
-      uint16_t nd[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      S c[8];
+      uint16_t nd[kSPT][8];
+      S c[kSPT][8];
+      uint8_t rk[kSPT][8];
 #pragma unroll
-      for (int a = 0; a < 8; ++a) c[a] = S(0);
-      if (valid) hex_loads<S, TD>(g, stage, sT, kc, g.hex_kf != nullptr, tid, nd, c);
-      uint8_t rk[8];
+      for (int q = 0; q < kSPT; ++q) {
+        const int i = q * kTileThreads + tid;
+        const int s = g.part_hex_start[p] + b * kBatch + i;
+        const Curve<S> &kc = g.mats.m[(g.hex_region && valid[q]) ? g.hex_region[s] : 0].k;
 #pragma unroll
-      for (int a = 0; a < 8; ++a) rk[a] = 0xff;
-      if (MODE == kRanked && valid) {
-        const StageLayout<S> L(8, g.hex_kf != nullptr, true);
-        const uint2 w = reinterpret_cast<const uint2 *>(stage + L.rank)[tid];
+        for (int a = 0; a < 8; ++a) {
+          nd[q][a] = 0;
+          c[q][a] = S(0);
+          rk[q][a] = 0xff;
+        }
+        if (valid[q]) hex_loads<S, TD>(g, stage, sT, kc, g.hex_kf != nullptr, i, nd[q], c[q]);
+        if (MODE == kRanked && valid[q]) {
+          const StageLayout<S> L(8, g.hex_kf != nullptr, true);
+          const uint2 w = reinterpret_cast<const uint2 *>(stage + L.rank)[i];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          rk[a] = (w.x >> (8 * a)) & 0xff;
-          rk[a + 4] = (w.y >> (8 * a)) & 0xff;
+          for (int a = 0; a < 4; ++a) {
+            rk[q][a] = (w.x >> (8 * a)) & 0xff;
+            rk[q][a + 4] = (w.y >> (8 * a)) & 0xff;
+          }
         }
       }
       accumulate<S, 8, MODE>(acc, nd, c, nfree, valid, rk, g.max_phase_hex);
@@ -380,6 +396,10 @@ __global__ void __launch_bounds__(kTileThreads) k_tiled_step(const __grid_consta
     if (tid == 0 && j + kStages < nb) {
       fence_proxy_async();
       issue_batch(g, p, j + kStages, nbt, stage, &bars[st]);
+    }
+    if (++st == kStages) {
+      st = 0;
+      parity ^= 1u;
     }
   }
   __syncthreads();

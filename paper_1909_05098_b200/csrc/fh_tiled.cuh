@@ -4,7 +4,9 @@
 
 namespace fh {
 
-constexpr int kTileThreads = 256;  // == partition batch size B
+constexpr int kTileThreads = 256;  // threads per tile CTA
+constexpr int kSPT = 1;            // element slots per thread per batch (2 measured slower: smem)
+constexpr int kBatch = kTileThreads * kSPT;  // == partition batch size B
 constexpr int kMaxStages = 4;      // TMA ring depth limit (batches in flight per CTA)
 
 template <typename S>
@@ -56,9 +58,9 @@ struct TiledArgs {
 // bytes of one staged batch: conn16 [B][N] | G [6][B] | kf [B] | rank [B][N]
 template <typename S>
 inline int StageBytes(int N, bool has_kf, bool has_rank) {
-  int b = kTileThreads * N * 2 + 6 * kTileThreads * (int)sizeof(S);
-  if (has_kf) b += kTileThreads * (int)sizeof(S);
-  if (has_rank) b += kTileThreads * N;
+  int b = kBatch * N * 2 + 6 * kBatch * (int)sizeof(S);
+  if (has_kf) b += kBatch * (int)sizeof(S);
+  if (has_rank) b += kBatch * N;
   return (b + 15) & ~15;
 }
 

@@ -186,6 +186,9 @@ int fh_step_timed(fh_engine *e, int64_t nsteps, double dt, fh_report *rep, float
 int fh_step_host(fh_engine *e, const double *T_in, double *T_out, int64_t n, int64_t nsteps, double dt,
                  fh_report *rep);
 
+/* set the static extra nodal power (W, original numbering, n == V) */
+int fh_set_q_static(fh_engine *e, const double *q, int64_t n);
+
 /* replace the time-dependent volumetric sources (n <= 8) after creation */
 int fh_set_sources(fh_engine *e, const fh_source *sources, int32_t n);
 
@@ -224,6 +227,32 @@ int fh_get_node_order(fh_engine *e, int64_t *new_to_old, int64_t n);
  * caller broadcasts it (torch.distributed), every rank attaches. */
 int fh_nccl_unique_id(char *id128);
 int fh_attach_nccl(fh_engine *e, const char *id128, int32_t rank, int32_t world);
+
+/* Halo bookkeeping of a multi-domain engine (rank = domain_lo / width, world =
+ * n_domains / width).  Node ids in the original numbering; per-peer ranges
+ * [offs[q], offs[q+1]).  fh_halo_export/import move the current halo values
+ * through host memory: the exchange used when several ranks share one GPU
+ * (tests), where kernels must never wait on one another. */
+int fh_halo_info(fh_engine *e, int32_t *world, int32_t *rank, int32_t *n_peers, int64_t *n_send, int64_t *n_recv,
+                 int64_t *n_boundary_parts, int64_t *n_parts);
+int fh_halo_lists(fh_engine *e, int32_t *peers, int64_t *send_offs, int64_t *send_nodes, int64_t *recv_offs,
+                  int64_t *recv_nodes);
+int fh_halo_export(fh_engine *e, double *send_values);
+int fh_halo_import(fh_engine *e, const double *recv_values);
+int fh_get_owned(fh_engine *e, uint8_t *mask, int64_t n);
+
+/* Host-only partition plan (no GPU needed): the tile / domain / halo
+ * bookkeeping fh_create performs, for checking it bit for bit.  info[] =
+ * {n_parts, parts of rank, boundary parts of rank, peers, n_send, n_recv,
+ * node_lo, node_hi, corner_unique, max_phase_tet, max_phase_hex, n_slots,
+ * max_local_nodes}. */
+typedef struct fh_plan fh_plan;
+int fh_plan_create(const fh_mesh *mesh, const fh_boundary *boundary, const fh_options *opts, int32_t world,
+                   int32_t rank, fh_plan **out);
+int fh_plan_info(fh_plan *plan, int64_t *info, int32_t n_info);
+int fh_plan_arrays(fh_plan *plan, int64_t *new_to_old, int64_t *part_node_start, int32_t *peers, int64_t *send_offs,
+                   int64_t *send_nodes, int64_t *recv_offs, int64_t *recv_nodes);
+int fh_plan_destroy(fh_plan *plan);
 
 #ifdef __cplusplus
 }

@@ -85,9 +85,10 @@ EXPORTS = [
     "fh_last_error", "fh_version", "fh_device_count", "fh_eval_curve_nodes", "fh_lumped_capacity_nodes",
     "fh_element_mean_nodal", "fh_scatter_net_loads", "fh_nodal_update", "fh_create", "fh_destroy",
     "fh_set_temperature", "fh_get_temperature", "fh_get_inflow", "fh_reset_properties", "fh_step",
-    "fh_step_timed", "fh_step_host", "fh_set_sources", "fh_set_probes", "fh_get_probes", "fh_critical_dt", "fh_scatter_loads",
+    "fh_step_timed", "fh_step_host", "fh_set_q_static", "fh_set_sources", "fh_set_probes", "fh_get_probes", "fh_critical_dt", "fh_scatter_loads",
     "fh_get_precompute", "fh_get_layout", "fh_stream", "fh_get_node_order", "fh_nccl_unique_id",
-    "fh_attach_nccl",
+    "fh_attach_nccl", "fh_halo_info", "fh_halo_lists", "fh_halo_export", "fh_halo_import", "fh_get_owned",
+    "fh_plan_create", "fh_plan_info", "fh_plan_arrays", "fh_plan_destroy",
 ]
 
 _lib = None
@@ -116,6 +117,7 @@ def lib():
     L.fh_step_timed.argtypes = [C.c_void_p, C.c_int64, C.c_double, C.POINTER(FhReport), C.POINTER(C.c_float)]
     L.fh_step_host.argtypes =[C.c_void_p, f64p, f64p, C.c_int64, C.c_int64, C.c_double, C.POINTER(FhReport)]
     L.fh_set_sources.argtypes = [C.c_void_p, C.POINTER(FhSource), C.c_int32]
+    L.fh_set_q_static.argtypes = [C.c_void_p, f64p, C.c_int64]
     L.fh_set_probes.argtypes = [C.c_void_p, i64p, C.c_int64, C.c_int64, C.c_int64]
     L.fh_get_probes.argtypes = [C.c_void_p, f64p, C.c_int64, i64p]
     L.fh_critical_dt.argtypes = [C.c_void_p, f64p, C.c_int64, f64p]
@@ -130,6 +132,17 @@ def lib():
     L.fh_nodal_update.argtypes = [f64p, f64p, f64p, f64p, f64p, f64p, f64p, C.c_int64, C.c_double]
     L.fh_nccl_unique_id.argtypes = [C.c_char_p]
     L.fh_attach_nccl.argtypes = [C.c_void_p, C.c_char_p, C.c_int32, C.c_int32]
+    i32o = C.POINTER(C.c_int32)
+    L.fh_halo_info.argtypes = [C.c_void_p, i32o, i32o, i32o, i64p, i64p, i64p, i64p]
+    L.fh_halo_lists.argtypes = [C.c_void_p, i32p, i64p, i64p, i64p, i64p]
+    L.fh_halo_export.argtypes = [C.c_void_p, f64p]
+    L.fh_halo_import.argtypes = [C.c_void_p, f64p]
+    L.fh_get_owned.argtypes = [C.c_void_p, C.POINTER(C.c_uint8), C.c_int64]
+    L.fh_plan_create.argtypes = [C.POINTER(FhMesh), C.POINTER(FhBoundary), C.POINTER(FhOptions), C.c_int32,
+                                 C.c_int32, C.POINTER(C.c_void_p)]
+    L.fh_plan_info.argtypes = [C.c_void_p, i64p, C.c_int32]
+    L.fh_plan_arrays.argtypes = [C.c_void_p, i64p, i64p, i32p, i64p, i64p, i64p, i64p]
+    L.fh_plan_destroy.argtypes = [C.c_void_p]
     _lib = L
     return L
 

@@ -7,6 +7,7 @@
 #include <numeric>
 #include <type_traits>
 
+#include "fh_dist.h"
 #include "fh_tiled.cuh"
 
 using namespace fh;
@@ -133,6 +134,7 @@ struct TiledState {
   int cur = 0;
   size_t smem = 0;
   int n_parts_local = 0;
+  int n_boundary = 0;  // multi-GPU: leading entries of part_list that touch the halo
   int mode = 0;
 };
 
@@ -177,6 +179,14 @@ struct fh_engine {
   DBuf<int64_t> old_of_new, new_of_old;
   std::unique_ptr<TiledState<float>> tf;
   std::unique_ptr<TiledState<double>> tdd;
+  // multi-GPU halo exchange (fh_dist.cu)
+  Exchange X;
+  DBuf<int32_t> x_send, x_recv;
+  DBuf<char> x_sendbuf, x_recvbuf;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_packed = nullptr, ev_halo = nullptr;
+  bool halo_pending = false;
+  void *comm = nullptr;  // ncclComm_t
   // probes
   DBuf<int32_t> probes;
   int64_t n_probes = 0, probe_interval = 1, probe_cap = 0, n_rec = 0;
@@ -186,6 +196,10 @@ struct fh_engine {
   DBuf<double> crit_kbar, crit_lam;
 
   ~fh_engine() {
+    if (comm) nccl_comm_destroy(comm);
+    if (ev_packed) cudaEventDestroy(ev_packed);
+    if (ev_halo) cudaEventDestroy(ev_halo);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -364,13 +378,30 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   auto st = std::make_unique<TiledState<S>>();
   TiledArgs<S> &g = st->args;
   std::memset(&g, 0, sizeof(g));
-  // parts of this engine: domains [lo, hi)
-  const int dlo = std::max(0, o.domain_lo), dhi = o.domain_hi > 0 ? o.domain_hi : pin.n_domains;
-  const int p_lo = P.domain_part_start[dlo], p_hi = P.domain_part_start[dhi];
-  std::vector<int32_t> plist;
-  for (int p = p_lo; p < p_hi; ++p) plist.push_back(p);
+  // parts of this engine: domains [lo, hi) = rank `lo / width` of `D / width`
+  const int D = pin.n_domains;
+  const int dlo = std::max(0, o.domain_lo), dhi = o.domain_hi > 0 ? o.domain_hi : D;
+  const int width = dhi - dlo;
+  if (width < 1 || dhi > D || D % width != 0 || dlo % width != 0)
+    fail(FH_ERR_CONFIG, "domain range must be one of D/width equal blocks");
+  {
+    std::vector<uint8_t> is_dir(e->V, 0);
+    for (int64_t i : e->dir_nodes) is_dir[P.new_of_old[i]] = 1;
+    build_exchange(P, is_dir.data(), D, D / width, dlo / width, e->X);
+  }
+  const std::vector<int32_t> &plist = e->X.part_order;  // boundary tiles first
   st->n_parts_local = (int)plist.size();
+  st->n_boundary = e->X.world > 1 ? e->X.n_boundary : 0;
   st->part_list.upload(plist, s);
+  if (e->X.world > 1) {
+    e->x_send.upload(e->X.send_nodes, s);
+    e->x_recv.upload(e->X.recv_nodes, s);
+    e->x_sendbuf.alloc(sizeof(S) * std::max<size_t>(1, e->X.send_nodes.size()));
+    e->x_recvbuf.alloc(sizeof(S) * std::max<size_t>(1, e->X.recv_nodes.size()));
+    FH_CUDA(cudaStreamCreateWithFlags(&e->comm_stream, cudaStreamNonBlocking));
+    FH_CUDA(cudaEventCreateWithFlags(&e->ev_packed, cudaEventDisableTiming));
+    FH_CUDA(cudaEventCreateWithFlags(&e->ev_halo, cudaEventDisableTiming));
+  }
   std::vector<int32_t> robin_base(P.n_parts + 1, 0);
   for (int p = 0; p < P.n_parts; ++p) robin_base[p + 1] = robin_base[p] + (P.part_n_free[p] - P.part_robin_start[p]);
   st->part_node_start.upload(P.part_node_start, s);
@@ -596,8 +627,31 @@ void tiled_run(fh_engine *e, int64_t nsteps, double dt) {
       d.cy = (S)(src.x0[1] + src.vel[1] * t);
       d.cz = (S)(src.x0[2] + src.vel[2] * t);
     }
-    g.part_begin = 0;
-    tiled_step(g, st.n_parts_local, e->td, st.mode, st.smem, e->stream);
+    if (e->X.world == 1) {
+      g.part_begin = 0;
+      tiled_step(g, st.n_parts_local, e->td, st.mode, st.smem, e->stream);
+    } else {
+      // interior tiles need no halo: they run while the previous step's
+      // exchange is still in flight on the comm stream
+      g.part_begin = st.n_boundary;
+      tiled_step(g, st.n_parts_local - st.n_boundary, e->td, st.mode, st.smem, e->stream);
+      if (e->halo_pending) FH_CUDA(cudaStreamWaitEvent(e->stream, e->ev_halo, 0));
+      e->halo_pending = false;
+      g.part_begin = 0;
+      tiled_step(g, st.n_boundary, e->td, st.mode, st.smem, e->stream);
+      if (e->comm) {
+        S *sendbuf = reinterpret_cast<S *>(e->x_sendbuf.p);
+        S *recvbuf = reinterpret_cast<S *>(e->x_recvbuf.p);
+        halo_pack<S>(g.Tout, e->x_send.p, (int64_t)e->X.send_nodes.size(), sendbuf, e->stream);
+        FH_CUDA(cudaEventRecord(e->ev_packed, e->stream));
+        FH_CUDA(cudaStreamWaitEvent(e->comm_stream, e->ev_packed, 0));
+        nccl_exchange(e->comm, sendbuf, recvbuf, sizeof(S), e->X.peers, e->X.send_offs, e->X.recv_offs,
+                      e->comm_stream);
+        halo_unpack<S>(g.Tout, e->x_recv.p, (int64_t)e->X.recv_nodes.size(), recvbuf, e->comm_stream);
+        FH_CUDA(cudaEventRecord(e->ev_halo, e->comm_stream));
+        e->halo_pending = true;
+      }
+    }
     st.cur ^= 1;
     e->step_index += 1;
     e->time = (double)e->step_index * dt;
@@ -648,6 +702,12 @@ int do_step(fh_engine *e, int64_t nsteps, double dt, fh_report *rep, float *elap
     tiled_run<float>(e, nsteps, dt);
   else
     tiled_run<double>(e, nsteps, dt);
+  if (e->halo_pending) {  // the last step is complete once its halo has landed
+    FH_CUDA(cudaStreamWaitEvent(e->stream, e->ev_halo, 0));
+    e->halo_pending = false;
+  }
+  if (e->comm)  // every rank agrees on the first failing step
+    nccl_min_u64(e->comm, &e->flag.p->step, e->stream);
   if (elapsed_ms) {
     FH_CUDA(cudaEventRecord(ev[1], e->stream));
     FH_CUDA(cudaEventSynchronize(ev[1]));
@@ -985,6 +1045,38 @@ int fh_step_host(fh_engine *e, const double *T_in, double *T_out, int64_t n, int
   FH_API_END
 }
 
+int fh_set_q_static(fh_engine *e, const double *q, int64_t n) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (n != e->V) fail(FH_ERR_CONFIG, "q_static has the wrong length");
+  e->q_static.assign(q, q + n);
+  if (e->assembly == FH_ASSEMBLY_EXACT) {
+    e->qstat.upload(e->q_static, e->stream);
+    e->ex.q_static = e->qstat.p;
+  } else {
+    auto set = [&](auto &st) {
+      using S = std::remove_reference_t<decltype(*st.T[0].p)>;
+      if (!st.q_ext.p) {
+        st.q_ext.alloc(e->V);
+        st.args.q_ext = st.q_ext.p;
+      }
+      if (e->load_power.empty()) {
+        FH_CUDA(cudaMemcpyAsync(e->stage.p, q, sizeof(double) * n, cudaMemcpyHostToDevice, e->stream));
+        float *qf = nullptr;
+        double *qd = nullptr;
+        if constexpr (sizeof(S) == 4) qf = st.q_ext.p; else qd = st.q_ext.p;
+        k_to_new<<<nblk(e->V), kBlk, 0, e->stream>>>(e->stage.p, e->old_of_new.p, e->V, qf, qd, nullptr, nullptr);
+        FH_CUDA(cudaGetLastError());
+      } else {
+        e->qr_valid = false;  // loads + static power are recombined at the next step
+      }
+    };
+    if (e->precision == 32) set(*e->tf); else set(*e->tdd);
+  }
+  FH_CUDA(cudaStreamSynchronize(e->stream));
+  FH_API_END
+}
+
 int fh_set_sources(fh_engine *e, const fh_source *sources, int32_t n) {
   FH_API_BEGIN
   check_engine(e);
@@ -1280,18 +1372,183 @@ int fh_nodal_update(double *temps, const double *inflow, const double *capacity,
 }
 
 int fh_nccl_unique_id(char *id128) {
-  (void)id128;
-  g_last_error = "multi-GPU exchange is built in fh_dist.cu";
-  return FH_ERR_CONFIG;
+  FH_API_BEGIN
+  NcclUniqueId id;
+  nccl_unique_id(&id);
+  std::memcpy(id128, id.internal, sizeof(id.internal));
+  FH_API_END
 }
 
 int fh_attach_nccl(fh_engine *e, const char *id128, int32_t rank, int32_t world) {
-  (void)e;
-  (void)id128;
-  (void)rank;
-  (void)world;
-  g_last_error = "multi-GPU exchange is built in fh_dist.cu";
-  return FH_ERR_CONFIG;
+  FH_API_BEGIN
+  check_engine(e);
+  if (e->assembly != FH_ASSEMBLY_TILED) fail(FH_ERR_CONFIG, "multi-GPU needs TILED mode");
+  if (world != e->X.world || rank != e->X.rank)
+    fail(FH_ERR_CONFIG, "rank/world do not match the engine's domain range");
+  if (world > 1 && !e->comm) {
+    NcclUniqueId id;
+    std::memcpy(id.internal, id128, sizeof(id.internal));
+    e->comm = nccl_comm_init(id, rank, world);
+  }
+  FH_API_END
+}
+
+// halo bookkeeping of the engine (original node ids) and a host-side exchange
+// used when ranks share one GPU in tests (no kernels wait on one another)
+int fh_halo_info(fh_engine *e, int32_t *world, int32_t *rank, int32_t *n_peers, int64_t *n_send, int64_t *n_recv,
+                 int64_t *n_boundary_parts, int64_t *n_parts) {
+  FH_API_BEGIN
+  check_engine(e);
+  *world = e->X.world;
+  *rank = e->X.rank;
+  *n_peers = (int32_t)e->X.peers.size();
+  *n_send = (int64_t)e->X.send_nodes.size();
+  *n_recv = (int64_t)e->X.recv_nodes.size();
+  *n_boundary_parts = e->X.n_boundary;
+  *n_parts = (int64_t)e->X.part_order.size();
+  FH_API_END
+}
+
+int fh_halo_lists(fh_engine *e, int32_t *peers, int64_t *send_offs, int64_t *send_nodes, int64_t *recv_offs,
+                  int64_t *recv_nodes) {
+  FH_API_BEGIN
+  check_engine(e);
+  const Exchange &X = e->X;
+  for (size_t q = 0; q < X.peers.size(); ++q) peers[q] = X.peers[q];
+  for (size_t q = 0; q < X.send_offs.size(); ++q) send_offs[q] = X.send_offs[q];
+  for (size_t q = 0; q < X.recv_offs.size(); ++q) recv_offs[q] = X.recv_offs[q];
+  for (size_t q = 0; q < X.send_nodes.size(); ++q) send_nodes[q] = e->part.old_of_new[X.send_nodes[q]];
+  for (size_t q = 0; q < X.recv_nodes.size(); ++q) recv_nodes[q] = e->part.old_of_new[X.recv_nodes[q]];
+  FH_API_END
+}
+
+}  // extern "C"
+
+template <typename S>
+static void halo_host_io(fh_engine *e, double *out, const double *in) {
+  TiledState<S> &st = tstate<S>(e);
+  const bool exp = out != nullptr;
+  const std::vector<int32_t> &nodes = exp ? e->X.send_nodes : e->X.recv_nodes;
+  const int64_t n = (int64_t)nodes.size();
+  if (!n) return;
+  std::vector<S> h(n);
+  DBuf<S> buf;
+  buf.alloc(n);
+  const int32_t *idx = exp ? e->x_send.p : e->x_recv.p;
+  if (exp) {
+    halo_pack<S>(st.T[st.cur].p, idx, n, buf.p, e->stream);
+    FH_CUDA(cudaMemcpyAsync(h.data(), buf.p, sizeof(S) * n, cudaMemcpyDeviceToHost, e->stream));
+    FH_CUDA(cudaStreamSynchronize(e->stream));
+    for (int64_t q = 0; q < n; ++q) out[q] = (double)h[q];
+  } else {
+    for (int64_t q = 0; q < n; ++q) h[q] = (S)in[q];
+    FH_CUDA(cudaMemcpyAsync(buf.p, h.data(), sizeof(S) * n, cudaMemcpyHostToDevice, e->stream));
+    halo_unpack<S>(st.T[st.cur].p, idx, n, buf.p, e->stream);
+    FH_CUDA(cudaStreamSynchronize(e->stream));
+  }
+}
+
+extern "C" {
+
+int fh_halo_export(fh_engine *e, double *send_values) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (e->X.world < 2) fail(FH_ERR_CONFIG, "engine has no halo");
+  if (e->precision == 32) halo_host_io<float>(e, send_values, nullptr); else halo_host_io<double>(e, send_values, nullptr);
+  FH_API_END
+}
+
+int fh_halo_import(fh_engine *e, const double *recv_values) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (e->X.world < 2) fail(FH_ERR_CONFIG, "engine has no halo");
+  if (e->precision == 32) halo_host_io<float>(e, nullptr, recv_values); else halo_host_io<double>(e, nullptr, recv_values);
+  FH_API_END
+}
+
+// owned-node mask in the original numbering (1 = this engine updates / owns it)
+int fh_get_owned(fh_engine *e, uint8_t *mask, int64_t n) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (n != e->V) fail(FH_ERR_CONFIG, "output has the wrong length");
+  if (e->assembly == FH_ASSEMBLY_EXACT) {
+    std::memset(mask, 1, (size_t)n);
+  } else {
+    std::memset(mask, 0, (size_t)n);
+    for (int64_t v = e->X.node_lo; v < e->X.node_hi; ++v) mask[e->part.old_of_new[v]] = 1;
+  }
+  FH_API_END
+}
+
+// ---------------------------------------------------------------------------
+// host-only partition plan (no GPU): the bookkeeping of fh_create for a rank
+struct fh_plan {
+  Partition P;
+  Exchange X;
+};
+
+int fh_plan_create(const fh_mesh *mesh, const fh_boundary *bnd, const fh_options *opts, int32_t world, int32_t rank,
+                   fh_plan **out) {
+  FH_API_BEGIN
+  auto pl = std::make_unique<fh_plan>();
+  const int64_t V = mesh->n_nodes;
+  std::vector<uint8_t> cls(V, 0);
+  for (int64_t q = 0; q < bnd->n_robin; ++q) cls[bnd->robin_nodes[q]] = 1;
+  for (int64_t q = 0; q < bnd->n_dirichlet; ++q) cls[bnd->dirichlet_nodes[q]] = 2;
+  PartitionInput pin{};
+  pin.V = V;
+  pin.n_tet = mesh->n_tets;
+  pin.n_hex = mesh->n_hexes;
+  pin.xyz = mesh->coords;
+  pin.tets = mesh->tets;
+  pin.hexes = mesh->hexes;
+  pin.node_class = cls.data();
+  pin.target_part_nodes = opts->part_nodes > 0 ? opts->part_nodes : (opts->precision == 32 ? 1536 : 768);
+  pin.batch = kBatch;
+  pin.n_domains = std::max(1, opts->n_domains);
+  pin.slab_axis = opts->slab_axis;
+  build_partition(pin, pl->P);
+  std::vector<uint8_t> is_dir(V, 0);
+  for (int64_t q = 0; q < bnd->n_dirichlet; ++q) is_dir[pl->P.new_of_old[bnd->dirichlet_nodes[q]]] = 1;
+  build_exchange(pl->P, is_dir.data(), pin.n_domains, world, rank, pl->X);
+  *out = pl.release();
+  FH_API_END
+}
+
+int fh_plan_info(fh_plan *pl, int64_t *info, int32_t n_info) {
+  FH_API_BEGIN
+  const int64_t v[] = {pl->P.n_parts, pl->X.part_hi - pl->X.part_lo, pl->X.n_boundary, (int64_t)pl->X.peers.size(),
+                       (int64_t)pl->X.send_nodes.size(), (int64_t)pl->X.recv_nodes.size(), pl->X.node_lo,
+                       pl->X.node_hi, (int64_t)pl->P.corner_unique, pl->P.max_phase_tet, pl->P.max_phase_hex,
+                       (int64_t)(pl->P.tet_slot_elem.size() + pl->P.hex_slot_elem.size()), pl->P.max_local_nodes};
+  for (int q = 0; q < n_info && q < (int)(sizeof(v) / sizeof(v[0])); ++q) info[q] = v[q];
+  FH_API_END
+}
+
+int fh_plan_arrays(fh_plan *pl, int64_t *new_to_old, int64_t *part_node_start, int32_t *peers, int64_t *send_offs,
+                   int64_t *send_nodes, int64_t *recv_offs, int64_t *recv_nodes) {
+  FH_API_BEGIN
+  const Partition &P = pl->P;
+  const Exchange &X = pl->X;
+  if (new_to_old) std::memcpy(new_to_old, P.old_of_new.data(), sizeof(int64_t) * P.old_of_new.size());
+  if (part_node_start)
+    for (size_t q = 0; q < P.part_node_start.size(); ++q) part_node_start[q] = P.part_node_start[q];
+  if (peers)
+    for (size_t q = 0; q < X.peers.size(); ++q) peers[q] = X.peers[q];
+  if (send_offs)
+    for (size_t q = 0; q < X.send_offs.size(); ++q) send_offs[q] = X.send_offs[q];
+  if (recv_offs)
+    for (size_t q = 0; q < X.recv_offs.size(); ++q) recv_offs[q] = X.recv_offs[q];
+  if (send_nodes)
+    for (size_t q = 0; q < X.send_nodes.size(); ++q) send_nodes[q] = P.old_of_new[X.send_nodes[q]];
+  if (recv_nodes)
+    for (size_t q = 0; q < X.recv_nodes.size(); ++q) recv_nodes[q] = P.old_of_new[X.recv_nodes[q]];
+  FH_API_END
+}
+
+int fh_plan_destroy(fh_plan *pl) {
+  delete pl;
+  return FH_OK;
 }
 
 }  // extern "C"

@@ -152,6 +152,22 @@ struct Partition {
 
 void build_partition(const PartitionInput &in, Partition &out);
 
+// Multi-GPU halo bookkeeping for `rank` of `world` ranks; rank r owns domains
+// [r*D/W, (r+1)*D/W).  Lists hold new node ids, ascending; Dirichlet nodes are
+// never exchanged (their values are constant on every rank).
+struct Exchange {
+  int rank = 0, world = 1;
+  int part_lo = 0, part_hi = 0;      // parts owned by this rank
+  int64_t node_lo = 0, node_hi = 0;  // owned new node ids
+  std::vector<int32_t> peers;        // ranks we talk to, ascending
+  std::vector<int64_t> send_offs, recv_offs;  // per peer (size peers+1)
+  std::vector<int32_t> send_nodes, recv_nodes;
+  std::vector<int32_t> part_order;   // owned parts: boundary parts first, then interior
+  int n_boundary = 0;
+};
+void build_exchange(const Partition &P, const uint8_t *is_dirichlet_new, int n_domains, int world, int rank,
+                    Exchange &X);
+
 // node -> incident conn positions (ascending), positions of the flat
 // tets-then-hexes connectivity (exact order of the reference's conn_data)
 void build_node_csr(int64_t V, int64_t n_tet, const int64_t *tets, int64_t n_hex, const int64_t *hexes,

@@ -325,3 +325,73 @@ void build_partition(const PartitionInput &in, Partition &P) {
 }
 
 }  // namespace fh
+
+namespace fh {
+
+// See fh_internal.h.  Every rank runs this on the same partition, so the
+// send list of r towards q is, element for element, the recv list of q from r.
+void build_exchange(const Partition &P, const uint8_t *is_dir, int n_domains, int world, int rank, Exchange &X) {
+  const int D = std::max(1, n_domains);
+  if (world < 1 || D % world != 0) fail(FH_ERR_CONFIG, "n_domains must be a multiple of the rank count");
+  X = Exchange{};
+  X.rank = rank;
+  X.world = world;
+  auto dom_lo = [&](int r) { return r * (D / world); };
+  X.part_lo = P.domain_part_start[dom_lo(rank)];
+  X.part_hi = P.domain_part_start[dom_lo(rank + 1)];
+  X.node_lo = P.part_node_start[X.part_lo];
+  X.node_hi = P.part_node_start[X.part_hi];
+  // rank owning a new node id
+  std::vector<int64_t> rank_node_start(world + 1);
+  for (int r = 0; r <= world; ++r) rank_node_start[r] = P.part_node_start[P.domain_part_start[dom_lo(r)]];
+  auto owner = [&](int64_t n) {
+    return (int)(std::upper_bound(rank_node_start.begin(), rank_node_start.end(), n) - rank_node_start.begin()) - 1;
+  };
+  // recv: remote, non-Dirichlet halo nodes of my parts; send: my nodes in the
+  // halo of any other rank's parts
+  std::vector<std::vector<int32_t>> recv(world), send(world);
+  std::vector<uint8_t> boundary(P.n_parts, 0);
+  for (int p = 0; p < P.n_parts; ++p) {
+    const int pr = owner(P.part_node_start[p]);
+    for (int32_t q = P.part_halo_start[p]; q < P.part_halo_start[p + 1]; ++q) {
+      const int32_t n = P.halo_nodes[q];
+      if (is_dir && is_dir[n]) continue;
+      const int nr = owner(n);
+      if (nr == pr) continue;
+      if (pr == rank) {
+        recv[nr].push_back(n);
+        boundary[p] = 1;
+      } else if (nr == rank) {
+        send[pr].push_back(n);
+      }
+    }
+  }
+  // parts owning a sent node are boundary parts too
+  std::vector<int32_t> part_of(X.node_hi - X.node_lo);
+  for (int p = X.part_lo; p < X.part_hi; ++p)
+    for (int32_t n = P.part_node_start[p]; n < P.part_node_start[p + 1]; ++n) part_of[n - X.node_lo] = p;
+  X.send_offs.assign(1, 0);
+  X.recv_offs.assign(1, 0);
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) continue;
+    auto &s = send[r], &v = recv[r];
+    std::sort(s.begin(), s.end());
+    s.erase(std::unique(s.begin(), s.end()), s.end());
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    if (s.empty() && v.empty()) continue;
+    X.peers.push_back(r);
+    for (int32_t n : s) boundary[part_of[n - X.node_lo]] = 1;
+    X.send_nodes.insert(X.send_nodes.end(), s.begin(), s.end());
+    X.recv_nodes.insert(X.recv_nodes.end(), v.begin(), v.end());
+    X.send_offs.push_back((int64_t)X.send_nodes.size());
+    X.recv_offs.push_back((int64_t)X.recv_nodes.size());
+  }
+  for (int p = X.part_lo; p < X.part_hi; ++p)
+    if (boundary[p]) X.part_order.push_back(p);
+  X.n_boundary = (int)X.part_order.size();
+  for (int p = X.part_lo; p < X.part_hi; ++p)
+    if (!boundary[p]) X.part_order.push_back(p);
+}
+
+}  // namespace fh

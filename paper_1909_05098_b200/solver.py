@@ -215,6 +215,77 @@ def _source_array(sources):
     return arr
 
 
+def native_inputs(mesh, bnd, materials, *, sources=(), robin=(), kfactor=None, element_region=None,
+                  td_mode=False, precision=64, assembly="exact", runaway_limit=DEFAULT_RUNAWAY_LIMIT, device=0,
+                  part_nodes=0, n_domains=1, domains=None, slab_axis=-1):
+    """C-ABI descriptors (fh_mesh, fh_boundary, fh_options) for a problem.
+
+    Returns (mesh, boundary, options, keep, robin) -- ``keep`` holds the numpy
+    arrays the descriptors point into; it must outlive every native call.
+    """
+    keep = []
+    nodes, tets, hexes = N.f64(mesh.nodes), N.i64(mesh.tets), N.i64(mesh.hexes)
+    keep += [nodes, tets, hexes]
+    fm = N.FhMesh(mesh.n_nodes, N.ptr(nodes), tets.shape[0], N.ptr(tets, N.i64p), hexes.shape[0],
+                  N.ptr(hexes, N.i64p))
+    fb = N.FhBoundary()
+    dn, dv = N.i64(bnd.dirichlet_nodes), N.f64(bnd.dirichlet_values)
+    keep += [dn, dv]
+    fb.n_dirichlet, fb.dirichlet_nodes, fb.dirichlet_values = dn.size, N.ptr(dn, N.i64p), N.ptr(dv)
+    if bnd.loads:
+        offs = np.zeros(len(bnd.loads) + 1, np.int64)
+        for i, ld in enumerate(bnd.loads):
+            offs[i + 1] = offs[i] + ld[0].size
+        lnodes = N.i64(np.concatenate([ld[0] for ld in bnd.loads]))
+        lp = N.f64([ld[1] for ld in bnd.loads])
+        l0 = N.f64([ld[2] for ld in bnd.loads])
+        l1 = N.f64([ld[3] for ld in bnd.loads])
+        keep += [offs, lnodes, lp, l0, l1]
+        fb.n_loads, fb.load_offsets, fb.load_nodes = len(bnd.loads), N.ptr(offs, N.i64p), N.ptr(lnodes, N.i64p)
+        fb.load_power, fb.load_t0, fb.load_t1 = N.ptr(lp), N.ptr(l0), N.ptr(l1)
+    dyn = [s for s in sources if not s.is_static]
+    if dyn:
+        arr = _source_array(dyn)
+        keep.append(arr)
+        fb.n_sources, fb.sources = len(dyn), C.cast(arr, C.POINTER(N.FhSource))
+    robin_out = None
+    robin = tuple(robin) if isinstance(robin, (list, tuple)) else (robin,)
+    if robin:
+        parts = [robin_lumps(mesh, r, exclude=bnd.dirichlet_nodes) for r in robin if isinstance(r, RobinSpec)]
+        rn = np.concatenate([p[0] for p in parts])
+        ra = np.concatenate([p[1] for p in parts])
+        rb = np.concatenate([p[2] for p in parts])
+        if np.unique(rn).size != rn.size:
+            raise ConfigError("a node is in more than one Robin set")
+        rn, ra, rb = N.i64(rn), N.f64(ra), N.f64(rb)
+        keep += [rn, ra, rb]
+        robin_out = (rn, ra, rb)
+        fb.n_robin, fb.robin_nodes, fb.robin_hA, fb.robin_hAT = rn.size, N.ptr(rn, N.i64p), N.ptr(ra), N.ptr(rb)
+    mats = (N.FhMaterial * len(materials))()
+    for r, m in enumerate(materials):
+        mats[r] = N.FhMaterial(_curve(m.density, keep), _curve(m.specific_heat, keep), _curve(m.conductivity, keep),
+                               _curve(m.perfusion_curve, keep), m.perfusion_rate, m.blood_specific_heat,
+                               m.arterial_temperature, m.metabolic_rate)
+    keep.append(mats)
+    fo = N.FhOptions()
+    fo.precision, fo.assembly, fo.td_mode, fo.device = int(precision), N.ASSEMBLY[assembly], int(td_mode), int(device)
+    fo.runaway_limit = float(runaway_limit)
+    fo.n_materials, fo.materials = len(materials), C.cast(mats, C.POINTER(N.FhMaterial))
+    if element_region is not None:
+        er = np.ascontiguousarray(element_region, dtype=np.int32)
+        keep.append(er)
+        fo.element_region = N.ptr(er, N.i32p)
+    if kfactor is not None:
+        kf = N.f64(kfactor)
+        keep.append(kf)
+        fo.element_kfactor = N.ptr(kf)
+    fo.part_nodes = int(part_nodes)
+    fo.n_domains = int(n_domains)
+    lo, hi = domains if domains is not None else (0, int(n_domains))
+    fo.domain_lo, fo.domain_hi, fo.slab_axis = int(lo), int(hi), int(slab_axis)
+    return fm, fb, fo, keep, robin_out
+
+
 class ExplicitEngine:
     """GPU-resident explicit engine for one model (solver.py:243-519)."""
 
@@ -242,86 +313,24 @@ class ExplicitEngine:
         self.sources = tuple(sources)
         self._packed = None
         N.require_gpu()
-        keep = []
+        fm, fb, fo, keep, self.robin = native_inputs(
+            mesh, self.boundary, self.materials, sources=self.sources, robin=robin, kfactor=kfactor,
+            element_region=element_region, td_mode=self.td_mode, precision=self.precision, assembly=assembly,
+            runaway_limit=self.runaway_limit, device=device, part_nodes=part_nodes, n_domains=n_domains,
+            domains=domains, slab_axis=slab_axis)
         self._keep = keep
-        nodes, tets, hexes = N.f64(mesh.nodes), N.i64(mesh.tets), N.i64(mesh.hexes)
-        keep += [nodes, tets, hexes]
-        fm = N.FhMesh(mesh.n_nodes, N.ptr(nodes), tets.shape[0], N.ptr(tets, N.i64p), hexes.shape[0],
-                      N.ptr(hexes, N.i64p))
-        fb = N.FhBoundary()
-        bnd = self.boundary
-        dn, dv = N.i64(bnd.dirichlet_nodes), N.f64(bnd.dirichlet_values)
-        keep += [dn, dv]
-        fb.n_dirichlet, fb.dirichlet_nodes, fb.dirichlet_values = dn.size, N.ptr(dn, N.i64p), N.ptr(dv)
-        if bnd.loads:
-            offs = np.zeros(len(bnd.loads) + 1, np.int64)
-            for i, ld in enumerate(bnd.loads):
-                offs[i + 1] = offs[i] + ld[0].size
-            lnodes = N.i64(np.concatenate([ld[0] for ld in bnd.loads]))
-            lp = N.f64([ld[1] for ld in bnd.loads])
-            l0 = N.f64([ld[2] for ld in bnd.loads])
-            l1 = N.f64([ld[3] for ld in bnd.loads])
-            keep += [offs, lnodes, lp, l0, l1]
-            fb.n_loads, fb.load_offsets, fb.load_nodes = len(bnd.loads), N.ptr(offs, N.i64p), N.ptr(lnodes, N.i64p)
-            fb.load_power, fb.load_t0, fb.load_t1 = N.ptr(lp), N.ptr(l0), N.ptr(l1)
-        dyn = [s for s in self.sources if not s.is_static]
-        if dyn:
-            arr = _source_array(dyn)
-            keep.append(arr)
-            fb.n_sources, fb.sources = len(dyn), C.cast(arr, C.POINTER(N.FhSource))
-        self.robin = None
-        robin = tuple(robin) if isinstance(robin, (list, tuple)) else (robin,)
-        if robin:
-            parts = [robin_lumps(mesh, r, exclude=bnd.dirichlet_nodes) for r in robin if isinstance(r, RobinSpec)]
-            rn = np.concatenate([p[0] for p in parts])
-            ra = np.concatenate([p[1] for p in parts])
-            rb = np.concatenate([p[2] for p in parts])
-            if np.unique(rn).size != rn.size:
-                raise ConfigError("a node is in more than one Robin set")
-            rn, ra, rb = N.i64(rn), N.f64(ra), N.f64(rb)
-            keep += [rn, ra, rb]
-            self.robin = (rn, ra, rb)
-            fb.n_robin, fb.robin_nodes, fb.robin_hA, fb.robin_hAT = rn.size, N.ptr(rn, N.i64p), N.ptr(ra), N.ptr(rb)
-        mats = (N.FhMaterial * len(self.materials))()
-        for r, m in enumerate(self.materials):
-            mats[r] = N.FhMaterial(_curve(m.density, keep), _curve(m.specific_heat, keep),
-                                   _curve(m.conductivity, keep), _curve(m.perfusion_curve, keep),
-                                   m.perfusion_rate, m.blood_specific_heat, m.arterial_temperature,
-                                   m.metabolic_rate)
-        keep.append(mats)
-        fo = N.FhOptions()
-        fo.precision, fo.assembly, fo.td_mode, fo.device = self.precision, N.ASSEMBLY[assembly], int(self.td_mode), device
-        fo.runaway_limit = self.runaway_limit
-        fo.n_materials, fo.materials = len(self.materials), C.cast(mats, C.POINTER(N.FhMaterial))
-        if element_region is not None:
-            er = np.ascontiguousarray(element_region, dtype=np.int32)
-            keep.append(er)
-            fo.element_region = N.ptr(er, N.i32p)
-        if kfactor is not None:
-            kf = N.f64(kfactor)
-            keep.append(kf)
-            fo.element_kfactor = N.ptr(kf)
-        fo.part_nodes = int(part_nodes)
-        fo.n_domains = int(n_domains)
-        lo, hi = domains if domains is not None else (0, int(n_domains))
-        fo.domain_lo, fo.domain_hi, fo.slab_axis = int(lo), int(hi), int(slab_axis)
-        # static sources need the lumped volumes: create, read volumes, recreate
-        static = [s for s in self.sources if s.is_static]
         self._h = None
         handle = C.c_void_p()
-        if static:
-            N.check(N.lib().fh_create(C.byref(fm), C.byref(fb), C.byref(fo), C.byref(handle)))
-            vols = np.empty(mesh.n_nodes)
-            N.check(N.lib().fh_get_precompute(handle, N.ptr(vols), None))
-            N.lib().fh_destroy(handle)
-            qs = N.f64(static_nodal_power(static, mesh.nodes, vols))
-            keep.append(qs)
-            fb.q_static = N.ptr(qs)
-            self.q_static = qs
-        else:
-            self.q_static = None
         N.check(N.lib().fh_create(C.byref(fm), C.byref(fb), C.byref(fo), C.byref(handle)))
         self._h = handle
+        # static sources are lumped with the device-computed volumes: Q(x_i) * v_i
+        static = [s for s in self.sources if s.is_static]
+        self.q_static = None
+        if static:
+            vols = np.empty(mesh.n_nodes)
+            N.check(N.lib().fh_get_precompute(handle, N.ptr(vols), None))
+            self.q_static = N.f64(static_nodal_power(static, mesh.nodes, vols))
+            N.check(N.lib().fh_set_q_static(handle, N.ptr(self.q_static), mesh.n_nodes))
         self._L = N.lib()
         vols = np.empty(mesh.n_nodes)
         N.check(self._L.fh_get_precompute(self._h, N.ptr(vols), None))
@@ -333,6 +342,44 @@ class ExplicitEngine:
         if h:
             self._L.fh_destroy(h)
             self._h = None
+
+    # -- device state / multi-domain helpers ------------------------------------
+    def temperature(self) -> np.ndarray:
+        """Current device field (original numbering, float64)."""
+        T = np.empty(self.n_nodes)
+        N.check(self._L.fh_get_temperature(self._h, N.ptr(T), T.size))
+        return T
+
+    def owned_mask(self) -> np.ndarray:
+        m = np.zeros(self.n_nodes, np.uint8)
+        N.check(self._L.fh_get_owned(self._h, m.ctypes.data_as(C.POINTER(C.c_uint8)), m.size))
+        return m.astype(bool)
+
+    def halo_info(self) -> dict:
+        w, r, npeer = C.c_int32(), C.c_int32(), C.c_int32()
+        ns, nr, nb, nparts = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        N.check(self._L.fh_halo_info(self._h, C.byref(w), C.byref(r), C.byref(npeer), C.byref(ns), C.byref(nr),
+                                     C.byref(nb), C.byref(nparts)))
+        return {"world": w.value, "rank": r.value, "n_peers": npeer.value, "n_send": ns.value,
+                "n_recv": nr.value, "boundary_parts": nb.value, "parts": nparts.value}
+
+    def halo_lists(self):
+        i = self.halo_info()
+        peers = np.empty(i["n_peers"], np.int32)
+        so, ro = np.empty(i["n_peers"] + 1, np.int64), np.empty(i["n_peers"] + 1, np.int64)
+        sn, rn = np.empty(i["n_send"], np.int64), np.empty(i["n_recv"], np.int64)
+        N.check(self._L.fh_halo_lists(self._h, N.ptr(peers, N.i32p), N.ptr(so, N.i64p), N.ptr(sn, N.i64p),
+                                      N.ptr(ro, N.i64p), N.ptr(rn, N.i64p)))
+        return peers, so, sn, ro, rn
+
+    def halo_export(self) -> np.ndarray:
+        out = np.empty(self.halo_info()["n_send"])
+        N.check(self._L.fh_halo_export(self._h, N.ptr(out)))
+        return out
+
+    def halo_import(self, values) -> None:
+        v = N.f64(values)
+        N.check(self._L.fh_halo_import(self._h, N.ptr(v)))
 
     def set_sources(self, sources) -> None:
         """Replace the time-dependent sources (static ones stay folded into q_static)."""

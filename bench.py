@@ -194,14 +194,26 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        raise SystemExit("multi-GPU bench: see bench_dist (not built in this revision)")
     torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     prob = make_problem(args.config, args.divisions, args.precision)
     mesh = prob.mesh
     t_setup = time.perf_counter()
-    eng = fh.ExplicitEngine(mesh, prob.material, prob.boundary, assembly="tiled", device=local,
-                            part_nodes=args.part_nodes, **prob.engine_kwargs())
+    if world > 1:
+        from paper_1909_05098_b200.dist import make_engine
+
+        # cfg4 is slab-partitioned along z (BASELINE.json); 8 domains so that the
+        # tiles -- and therefore the results -- are the same for 1/2/4/8 GPUs
+        eng = make_engine(mesh, prob.material, prob.boundary, rank=rank, world=world, device=local,
+                          n_domains=8, slab_axis=2 if prob.name == "cfg4" else -1, part_nodes=args.part_nodes,
+                          **prob.engine_kwargs())
+    else:  # same tiles as the multi-GPU runs: one engine owning all 8 domains
+        eng = fh.ExplicitEngine(mesh, prob.material, prob.boundary, assembly="tiled", device=local,
+                                part_nodes=args.part_nodes, n_domains=8,
+                                slab_axis=2 if prob.name == "cfg4" else -1, **prob.engine_kwargs())
     t_setup = time.perf_counter() - t_setup
     dt = 0.9 * eng.critical_dt(37.0)
     if prob.name == "cfg4":  # moving source: traverse the seeded segment over the run
@@ -223,15 +235,24 @@ def main():
     sampler.start()
     time.sleep(0.3)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     wall0 = time.time()
     elapsed = C.c_float(0.0)
     # CUDA events recorded on the engine's launch stream around the K launches
     rc = L.fh_step_timed(h, args.steps, dt, C.byref(rep), C.byref(elapsed))
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     wall1 = time.time()
     N.check(rc)
     del stream
     ms_total = float(elapsed.value)
+    if world > 1:  # max over ranks
+        t = torch.tensor([ms_total], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
     time.sleep(0.15)
     sampler.stop()
     clocks = sampler.summary(wall0, wall1)
@@ -240,25 +261,33 @@ def main():
     ms = ms_total / args.steps
     value = E * args.steps / (ms_total / 1e3)
     peak, peak_kind = peaks()
-    achieved = lay["canonical_bytes"] / (ms / 1e3) / 1e9
+    # per GPU: the canonical bytes of this GPU's share of the mesh
+    achieved = lay["canonical_bytes"] / world / (ms / 1e3) / 1e9
     # e2e: through the public C ABI with pinned host buffers, one step per call
+    # (the full field goes host->device and back every step, on every rank)
     Tin = torch.empty(mesh.n_nodes, dtype=torch.float64, pin_memory=True)
     Tout = torch.empty(mesh.n_nodes, dtype=torch.float64, pin_memory=True)
     Tin.numpy()[:] = T
     p_in = C.cast(C.c_void_p(Tin.data_ptr()), N.f64p)
     p_out = C.cast(C.c_void_p(Tout.data_ptr()), N.f64p)
     N.check(L.fh_step_host(h, p_in, p_out, T.size, 1, dt, C.byref(rep)))
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
         N.check(L.fh_step_host(h, p_in, p_out, T.size, 1, dt, C.byref(rep)))
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
             traffic = json.load(f).get(args.config)
     cpu = None
-    if not args.no_cpu_baseline and rank == 0:
+    if not args.no_cpu_baseline and rank == 0 and world == 1:
         div = args.cpu_sample_div or {"cfg4": 96, "cfg3": 40, "cfg1": 20, "cfg2": 20}[args.config]
         rate, el, elem, threads = cpu_oracle_rate(args.config, div, 3)
         cpu = {"value": rate, "unit": "element-steps/s", "cores": threads, "kind": "port",
@@ -267,10 +296,12 @@ def main():
     line = {
         "metric": "element-steps/sec", "value": value, "unit": "element-steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if prob.precision == 32 else "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32" if prob.precision == 32 else "f64",
         "data": "synthetic (seeded, BASELINE.json shapes)",
         "config": {"workload": prob.name, "elements": E, "nodes": mesh.n_nodes, "td": prob.td_mode,
                    "assembly": "tiled", "parts": lay["n_parts"], "slots": lay["n_slots"],
+                   "parallelism": f"{world} GPU domain decomposition (8 z-slab domains, NCCL halo exchange)"
+                   if world > 1 else "1 GPU",
                    "l2": "per-step input > 126 MB L2 (no flush needed)", "dt_s": dt, "setup_s": t_setup},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_kind": peak_kind,
@@ -278,11 +309,16 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": E / e2e_s, "unit": "element-steps/s", "h2d_bytes_per_step": 8 * mesh.n_nodes,
                 "d2h_bytes_per_step": 8 * mesh.n_nodes},
-        "gpu_launches": args.steps * lay["kernels_per_step"],
+        # per rank: 1 fused step kernel (N=1); interior + boundary tiles + halo pack/unpack (N>1)
+        "gpu_launches": args.steps * (lay["kernels_per_step"] if world == 1 else 4),
         "clocks": clocks,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        del eng
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

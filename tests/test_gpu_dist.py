@@ -30,7 +30,7 @@ def test_two_ranks_match_single_engine_bitwise(prec, slab):
     mat = fh.TissueMaterial(density=fh.make_constant(1060.0), specific_heat=fh.linear_law(3600.0, -0.0005, 37.0),
                             conductivity=fh.linear_law(0.5, 0.0013, 37.0), perfusion_rate=0.525,
                             blood_specific_heat=3640.0, metabolic_rate=420.0)
-    bnd = fh.BoundarySpec(dirichlet=(("z0", 37.0), ("x0", 40.0)))
+    bnd = fh.BoundarySpec(dirichlet=(("z0", 37.0), ("z1", 40.0)))
     src = (fh.GaussianSource(amp=5e6, sigma=0.01, x0=(0.05, 0.05, 0.05)),)
     kw = dict(precision=prec, part_nodes=200, n_domains=8, slab_axis=slab, sources=src)
     ref = fh.ExplicitEngine(mesh, mat, bnd, assembly="tiled", **kw)

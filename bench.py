@@ -128,7 +128,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_oracle_rate(name, divisions, steps, threads=None):
+def cpu_oracle_rate(name, divisions, steps, threads=None, per_step=False):
     """Time the CPU oracle (restated reference path) on a bounded sample."""
     from oracle import oracle as orc
 
@@ -149,6 +149,13 @@ def cpu_oracle_rate(name, divisions, steps, threads=None):
     ora.initial_state(37.0)
     dt = 0.9 * ora.critical_dt(np.full(mesh.n_nodes, 37.0))
     ora.step(dt, 1)  # warm-up
+    if per_step:
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            ora.step(dt, 1)
+            times.append(time.perf_counter() - t0)
+        return times, mesh.n_elements, orc.max_threads()
     t0 = time.perf_counter()
     ora.step(dt, steps)
     el = time.perf_counter() - t0
@@ -160,20 +167,18 @@ def run_reference(args):
     if rank != 0:
         return
     div = args.cpu_sample_div or {"cfg4": 96, "cfg3": 40, "cfg1": 20, "cfg2": 20}[args.config]
-    per_step = []
-    elem = 0
-    for i in range(args.warmup + args.steps):
-        rate, el, elem, threads = cpu_oracle_rate(args.config, div, 1)
-        if i >= args.warmup:
-            per_step.append(el)
+    # warm-up steps inside cpu_oracle_rate: 1 + W, then K timed steps
+    times, elem, threads = cpu_oracle_rate(args.config, div, args.warmup + args.steps, per_step=True)
+    per_step = times[args.warmup:]
     tot = sum(per_step)
     value = elem * len(per_step) / tot
-    sample = f"{args.config}-family mesh at {div}^3 cells ({elem} elements), one oracle step per bench step"
+    sample = (f"{args.config}-family mesh at {div}^3 cells ({elem} elements; the full workload is sampled "
+              f"per element), one oracle step (oracle/fh_oracle.c, reference op order, OpenMP) per bench step")
     line = {
         "impl": "reference", "metric": "element-steps/sec", "value": value, "unit": "element-steps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(per_step),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "sample_divisions": div},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "sample_divisions": div, "elements_sampled": elem},
         "cpu_baseline": {"value": value, "unit": "element-steps/s", "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "element-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

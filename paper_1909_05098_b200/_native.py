@@ -15,7 +15,7 @@ import numpy as np
 from .errors import DeviceError, FedheatError, raise_for_status
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfedheat_b200.so")
+LIB_PATH = os.environ.get("FH_LIB") or os.path.join(_HERE, "libfedheat_b200.so")
 MAX_KNOTS = 32
 CHUNK_SIZE = 4096
 

@@ -130,6 +130,7 @@ struct TiledState {
   DBuf<int32_t> tet_conn, hex_conn, tet_slot_elem, hex_slot_elem;
   DBuf<S> tet_G, hex_G, tet_kf, hex_kf, tet_kbar, hex_kbar;
   DBuf<uint8_t> tet_rank, hex_rank, tet_region, hex_region, node_region;
+  DBuf<uint8_t> tet_phase, hex_phase, tet_bnph, hex_bnph;
   DBuf<S> T[2], vol, cap, kb, q_ext, xyz, robin_hA, robin_hAT;
   int cur = 0;
   size_t smem = 0;
@@ -422,9 +423,24 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   }
   st->tet_slot_elem.upload(P.tet_slot_elem, s);
   st->hex_slot_elem.upload(P.hex_slot_elem, s);
-  if (!P.corner_unique) {
+  // accumulation mode (fh_tiled.cu): colour phases when the colouring fits,
+  // else ranked phases; FH_TILE_MODE (0..3) overrides (tuning knob)
+  int mode = P.colored_ok ? kModeColored : kModeRanked;
+  if (const char *env = getenv("FH_TILE_MODE")) {
+    const int m = atoi(env);
+    if (m == kModeRanked || (m == kModeColored && P.colored_ok) ||
+        ((m == kModeCornerPhase || m == kModeCornerSlot) && P.corner_unique))
+      mode = m;
+  }
+  if (mode == kModeRanked) {
     st->tet_rank.upload(P.tet_rank, s);
     st->hex_rank.upload(P.hex_rank, s);
+  }
+  if (mode == kModeColored) {
+    st->tet_phase.upload(P.tet_phase, s);
+    st->hex_phase.upload(P.hex_phase, s);
+    st->tet_bnph.upload(P.tet_batch_nph, s);
+    st->hex_bnph.upload(P.hex_batch_nph, s);
   }
   const int64_t nts = (int64_t)P.tet_slot_elem.size(), nhs = (int64_t)P.hex_slot_elem.size();
   st->tet_G.alloc(6 * nts);
@@ -516,6 +532,10 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.hex_G = st->hex_G.p;
   g.tet_kf = st->tet_kf.p;
   g.hex_kf = st->hex_kf.p;
+  g.tet_phase = st->tet_phase.p;
+  g.hex_phase = st->hex_phase.p;
+  g.tet_bnph = st->tet_bnph.p;
+  g.hex_bnph = st->hex_bnph.p;
   g.tet_rank = st->tet_rank.p;
   g.hex_rank = st->hex_rank.p;
   g.tet_region = st->tet_region.p;
@@ -537,18 +557,16 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   auto al = [](size_t b) { return (b + 127) & ~(size_t)127; };
   // accumulation mode: corner phases / corner slots need corner-unique tiles;
   // FH_TILE_MODE (0/1/2) and FH_TILE_STAGES override the defaults (tuning knobs)
-  st->mode = P.corner_unique ? kModeCornerPhase : kModeRanked;
-  if (const char *env = getenv("FH_TILE_MODE")) {
-    const int m = atoi(env);
-    if (m == kModeRanked || P.corner_unique) st->mode = m;
-  }
+  st->mode = mode;
   g.n_stages = 2;  // measured best on cfg4 (scripts/sweep.py)
   if (const char *env = getenv("FH_TILE_STAGES")) g.n_stages = std::min(kMaxStages, std::max(1, atoi(env)));
   g.smem_T = (int)al(2 * sizeof(S) * (size_t)std::max(1, P.max_local_nodes));
   g.smem_acc = (int)al(sizeof(S) * (st->mode == kModeCornerSlot ? 8 : 1) * (size_t)std::max(1, P.max_part_free));
   int stage = 0;
-  if (e->n_tet) stage = std::max(stage, StageBytes<S>(4, st->tet_kf.p || !e->td, !P.corner_unique));
-  if (e->n_hex) stage = std::max(stage, StageBytes<S>(8, st->hex_kf.p || !e->td, !P.corner_unique));
+  if (e->n_tet)
+    stage = std::max(stage, StageBytes<S>(4, st->tet_kf.p || !e->td, mode == kModeRanked, mode == kModeColored));
+  if (e->n_hex)
+    stage = std::max(stage, StageBytes<S>(8, st->hex_kf.p || !e->td, mode == kModeRanked, mode == kModeColored));
   g.stage_bytes = (int)al(stage);
   st->smem = (size_t)g.smem_T + g.smem_acc + (size_t)g.n_stages * g.stage_bytes;
   if (st->smem > 220 * 1024) fail(FH_ERR_CONFIG, "tile too large for shared memory; lower part_nodes");

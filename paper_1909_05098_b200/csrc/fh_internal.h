@@ -148,6 +148,12 @@ struct Partition {
   int max_part_nodes = 0;
   int max_local_nodes = 0;  // owned + halo
   int max_part_free = 0;
+  // colouring: slots of one colour share no updated node; slots are sorted by
+  // colour inside each tile, phase = colour index inside the batch
+  bool colored_ok = false;
+  int max_colors = 0, max_nph_tet = 0, max_nph_hex = 0;
+  std::vector<uint8_t> tet_color, hex_color, tet_phase, hex_phase;
+  std::vector<uint8_t> tet_batch_nph, hex_batch_nph;  // phases per batch (index = slot / B)
 };
 
 void build_partition(const PartitionInput &in, Partition &out);

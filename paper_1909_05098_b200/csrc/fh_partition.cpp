@@ -177,6 +177,7 @@ void build_partition(const PartitionInput &in, Partition &P) {
   std::vector<std::vector<int32_t>> tet_pp(P.n_parts), hex_pp(P.n_parts);
   build_slots<4>(in.n_tet, in.tets, 0, P, part_of_new, updatable_new, tet_pp);
   build_slots<8>(in.n_hex, in.hexes, in.n_tet, P, part_of_new, updatable_new, hex_pp);
+  std::vector<std::vector<uint8_t>> tet_color_pp, hex_color_pp;
   // order the slots of a part by their smallest corner id (new numbering), so
   // that neighbouring threads of a batch touch neighbouring nodes: the
   // shared-memory gathers and accumulations are then bank-conflict free
@@ -199,6 +200,55 @@ void build_partition(const PartitionInput &in, Partition &P) {
       sort_part(tet_pp[p], 4);
       sort_part(hex_pp[p], 8);
     }
+    // greedy colouring of each tile's slots: two slots of one colour never
+    // share a node the tile updates.  A stable sort by colour makes every
+    // batch span few colours -> few accumulation phases (kColored mode).
+    std::vector<uint64_t> used(P.max_part_nodes, 0);
+    std::vector<std::pair<int, int32_t>> ct;
+    P.colored_ok = true;
+    P.max_colors = 0;
+    auto colour_part = [&](std::vector<int32_t> &v, int N, int p) {
+      const int64_t n0 = P.part_node_start[p], nf = P.part_n_free[p];
+      ct.clear();
+      for (int32_t e : v) {
+        const int64_t *c = N == 4 ? in.tets + 4 * (int64_t)e : in.hexes + 8 * ((int64_t)e - in.n_tet);
+        uint64_t m = 0;
+        for (int a = 0; a < N; ++a) {
+          const int64_t loc = P.new_of_old[c[a]] - n0;
+          if (loc >= 0 && loc < nf) m |= used[loc];
+        }
+        if (~m == 0) {
+          P.colored_ok = false;
+          ct.emplace_back(63, e);
+          continue;
+        }
+        const int col = __builtin_ctzll(~m);
+        P.max_colors = std::max(P.max_colors, col + 1);
+        for (int a = 0; a < N; ++a) {
+          const int64_t loc = P.new_of_old[c[a]] - n0;
+          if (loc >= 0 && loc < nf) used[loc] |= (1ull << col);
+        }
+        ct.emplace_back(col, e);
+      }
+      for (int32_t e : v) {  // reset the masks of this tile
+        const int64_t *c = N == 4 ? in.tets + 4 * (int64_t)e : in.hexes + 8 * ((int64_t)e - in.n_tet);
+        for (int a = 0; a < N; ++a) {
+          const int64_t loc = P.new_of_old[c[a]] - n0;
+          if (loc >= 0 && loc < nf) used[loc] = 0;
+        }
+      }
+      std::stable_sort(ct.begin(), ct.end(), [](const auto &x, const auto &y) { return x.first < y.first; });
+      for (size_t q = 0; q < v.size(); ++q) v[q] = ct[q].second;
+      return ct;
+    };
+    P.tet_color.clear();
+    P.hex_color.clear();
+    tet_color_pp.assign(P.n_parts, {});
+    hex_color_pp.assign(P.n_parts, {});
+    for (int p = 0; p < P.n_parts; ++p) {
+      for (auto &x : colour_part(tet_pp[p], 4, p)) tet_color_pp[p].push_back((uint8_t)x.first);
+      for (auto &x : colour_part(hex_pp[p], 8, p)) hex_color_pp[p].push_back((uint8_t)x.first);
+    }
   }
   P.part_tet_start.assign(P.n_parts + 1, 0);
   P.part_hex_start.assign(P.n_parts + 1, 0);
@@ -214,9 +264,13 @@ void build_partition(const PartitionInput &in, Partition &P) {
   }
   P.tet_slot_elem.assign(P.part_tet_start.back(), -1);
   P.hex_slot_elem.assign(P.part_hex_start.back(), -1);
+  P.tet_color.assign(P.part_tet_start.back(), 0xff);
+  P.hex_color.assign(P.part_hex_start.back(), 0xff);
   for (int p = 0; p < P.n_parts; ++p) {
     std::copy(tet_pp[p].begin(), tet_pp[p].end(), P.tet_slot_elem.begin() + P.part_tet_start[p]);
     std::copy(hex_pp[p].begin(), hex_pp[p].end(), P.hex_slot_elem.begin() + P.part_hex_start[p]);
+    std::copy(tet_color_pp[p].begin(), tet_color_pp[p].end(), P.tet_color.begin() + P.part_tet_start[p]);
+    std::copy(hex_color_pp[p].begin(), hex_color_pp[p].end(), P.hex_color.begin() + P.part_hex_start[p]);
   }
   tet_pp.clear();
   hex_pp.clear();
@@ -322,6 +376,32 @@ void build_partition(const PartitionInput &in, Partition &P) {
   do_kind(4, P.part_tet_start, P.part_tet_count, P.tet_conn, P.tet_rank, P.max_phase_tet);
   do_kind(8, P.part_hex_start, P.part_hex_count, P.hex_conn, P.hex_rank, P.max_phase_hex);
   P.corner_unique = unique;
+  // 7. colour phases: phase of a slot = index of its colour among the colours
+  //    of its batch (colours are sorted, so each batch holds a contiguous run)
+  auto colour_phases = [&](const std::vector<int32_t> &starts, const std::vector<int32_t> &counts,
+                           const std::vector<uint8_t> &color, std::vector<uint8_t> &phase,
+                           std::vector<uint8_t> &batch_nph, int &max_nph) {
+    phase.assign(color.size(), 0);
+    batch_nph.assign(color.size() / B + 1, 0);
+    max_nph = 0;
+    for (int p = 0; p < P.n_parts; ++p) {
+      const int32_t s_end = starts[p] + counts[p];
+      for (int32_t b = starts[p]; b < s_end; b += B) {
+        const int32_t be = std::min(s_end, b + B);
+        int ph = 0;
+        for (int32_t s = b; s < be; ++s) {
+          if (s > b && color[s] != color[s - 1]) ++ph;
+          phase[s] = (uint8_t)ph;
+        }
+        batch_nph[b / B] = (uint8_t)(ph + 1);
+        max_nph = std::max(max_nph, ph + 1);
+      }
+    }
+  };
+  if (P.colored_ok) {
+    colour_phases(P.part_tet_start, P.part_tet_count, P.tet_color, P.tet_phase, P.tet_batch_nph, P.max_nph_tet);
+    colour_phases(P.part_hex_start, P.part_hex_count, P.hex_color, P.hex_phase, P.hex_batch_nph, P.max_nph_hex);
+  }
 }
 
 }  // namespace fh

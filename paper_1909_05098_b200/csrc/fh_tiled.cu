@@ -26,6 +26,13 @@ namespace fh {
 
 constexpr unsigned long long kNone = ~0ull;
 
+// minimum resident CTAs per SM requested from ptxas for the fp32 step kernel
+// (caps registers; the default is the measured best, see scripts/sweep.py)
+#ifndef FH_MIN_BLOCKS_F32
+#define FH_MIN_BLOCKS_F32 4
+#endif
+constexpr int kMinBlocksF32 = FH_MIN_BLOCKS_F32;
+
 // (T, k(T)) of a tile-local node, staged once per tile in shared memory
 template <typename S>
 struct __align__(2 * sizeof(S)) TK {
@@ -70,14 +77,13 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // stage layout for one batch of B slots of a kind with N corners
 template <typename S>
 struct StageLayout {
-  int conn, G, kf, rank, bytes;
+  int conn, G, kf, rank, phase;
   __host__ __device__ StageLayout(int N, bool has_kf, bool has_rank) {
     conn = 0;
     G = kBatch * N * 2;
     kf = G + 6 * kBatch * (int)sizeof(S);
     rank = kf + (has_kf ? kBatch * (int)sizeof(S) : 0);
-    bytes = rank + (has_rank ? kBatch * N : 0);
-    bytes = (bytes + 15) & ~15;
+    phase = rank + (has_rank ? kBatch * N : 0);  // colored mode only (no rank block then)
   }
 };
 
@@ -139,11 +145,15 @@ __device__ void issue_batch(const TiledArgs<S> &g, int p, int j, int nbt, unsign
   const S *G = tet ? g.tet_G : g.hex_G;
   const S *kf = tet ? g.tet_kf : g.hex_kf;
   const uint8_t *rank = tet ? g.tet_rank : g.hex_rank;
+  const uint8_t *phase = tet ? g.tet_phase : g.hex_phase;
   const StageLayout<S> L(N, kf != nullptr, rank != nullptr);
+  const int kp = (k + 15) & ~15;  // bulk copies move multiples of 16 bytes
   uint32_t bytes = (uint32_t)(kr * N * 2 + 6 * kr * sizeof(S));
   if (kf) bytes += kr * sizeof(S);
   if (rank) bytes += kr * N;
+  if (phase) bytes += kp;
   mbar_expect_tx(bar, bytes);
+  if (phase) bulk_g2s(stage + L.phase, phase + s0, kp, bar);
   bulk_g2s(stage + L.conn, conn + (size_t)N * s0, kr * N * 2, bar);
   const S *Gb = G + (size_t)(s0 / kBatch) * 6 * kBatch;
 #pragma unroll
@@ -232,7 +242,10 @@ __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned 
 //   kCornerSlot  corner-unique tiles: one accumulator row per corner, plain
 //                stores, summed in corner order at the node update (1 barrier)
 // Each thread carries kSPT slots of the batch (i = q * kTileThreads + tid).
-enum { kRanked = 0, kCornerPhase = 1, kCornerSlot = 2 };
+//   kColored     slots sorted by colour (no two slots of a colour share an
+//                updated node): phase = colour index inside the batch, so a
+//                batch needs as many barriers as it holds colours (1-2)
+enum { kRanked = 0, kCornerPhase = 1, kCornerSlot = 2, kColored = 3 };
 
 template <typename S, int N, int MODE>
 __device__ __forceinline__ void accumulate(S *acc, const uint16_t (&nd)[kSPT][N], const S (&c)[kSPT][N], int nfree,
@@ -269,7 +282,7 @@ __device__ __forceinline__ void accumulate(S *acc, const uint16_t (&nd)[kSPT][N]
   }
 }
 template <typename S, bool TD, int MODE>
-__global__ void __launch_bounds__(kTileThreads) k_tiled_step(const __grid_constant__ TiledArgs<S> g) {
+__global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 : 2) k_tiled_step(const __grid_constant__ TiledArgs<S> g) {
   extern __shared__ __align__(128) unsigned char smem[];
   TK<S> *sT = reinterpret_cast<TK<S> *>(smem);
   S *acc = reinterpret_cast<S *>(smem + g.smem_T);
@@ -362,8 +375,18 @@ __global__ void __launch_bounds__(kTileThreads) k_tiled_step(const __grid_consta
           const uint32_t w = reinterpret_cast<const uint32_t *>(stage + L.rank)[i];
           rk[q][0] = w & 0xff; rk[q][1] = (w >> 8) & 0xff; rk[q][2] = (w >> 16) & 0xff; rk[q][3] = w >> 24;
         }
+        if (MODE == kColored && valid[q]) {
+          const StageLayout<S> L(4, g.tet_kf != nullptr, false);
+          const uint8_t ph = stage[L.phase + i];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) rk[q][a] = ph;
+        }
       }
-      accumulate<S, 4, MODE>(acc, nd, c, nfree, valid, rk, g.max_phase_tet);
+      if (MODE == kColored)  // every corner of a slot is added in its colour's phase
+        accumulate<S, 4, kRanked>(acc, nd, c, nfree, valid, rk,
+                                  g.tet_bnph[(g.part_tet_start[p] + b * kBatch) / kBatch]);
+      else
+        accumulate<S, 4, MODE>(acc, nd, c, nfree, valid, rk, g.max_phase_tet);
     } else {
       uint16_t nd[kSPT][8];
       S c[kSPT][8];
@@ -389,8 +412,18 @@ __global__ void __launch_bounds__(kTileThreads) k_tiled_step(const __grid_consta
             rk[q][a + 4] = (w.y >> (8 * a)) & 0xff;
           }
         }
+        if (MODE == kColored && valid[q]) {
+          const StageLayout<S> L(8, g.hex_kf != nullptr, false);
+          const uint8_t ph = stage[L.phase + i];
+#pragma unroll
+          for (int a = 0; a < 8; ++a) rk[q][a] = ph;
+        }
       }
-      accumulate<S, 8, MODE>(acc, nd, c, nfree, valid, rk, g.max_phase_hex);
+      if (MODE == kColored)
+        accumulate<S, 8, kRanked>(acc, nd, c, nfree, valid, rk,
+                                  g.hex_bnph[(g.part_hex_start[p] + b * kBatch) / kBatch]);
+      else
+        accumulate<S, 8, MODE>(acc, nd, c, nfree, valid, rk, g.max_phase_hex);
     }
     // every thread passed the last phase barrier: the stage can be refilled
     if (tid == 0 && j + kStages < nb) {
@@ -467,12 +500,14 @@ template <typename S>
 void tiled_step(const TiledArgs<S> &g, int n_parts, bool td, int mode_sel, size_t smem, cudaStream_t s) {
   if (n_parts <= 0) return;
   using K = void (*)(TiledArgs<S>);
-  static const K table[2][3] = {
-      {k_tiled_step<S, false, kRanked>, k_tiled_step<S, false, kCornerPhase>, k_tiled_step<S, false, kCornerSlot>},
-      {k_tiled_step<S, true, kRanked>, k_tiled_step<S, true, kCornerPhase>, k_tiled_step<S, true, kCornerSlot>}};
-  const int mode = mode_sel < 0 || mode_sel > 2 ? 0 : mode_sel;
+  static const K table[2][4] = {
+      {k_tiled_step<S, false, kRanked>, k_tiled_step<S, false, kCornerPhase>, k_tiled_step<S, false, kCornerSlot>,
+       k_tiled_step<S, false, kColored>},
+      {k_tiled_step<S, true, kRanked>, k_tiled_step<S, true, kCornerPhase>, k_tiled_step<S, true, kCornerSlot>,
+       k_tiled_step<S, true, kColored>}};
+  const int mode = mode_sel < 0 || mode_sel > 3 ? 0 : mode_sel;
   const K kern = table[td ? 1 : 0][mode];
-  static size_t configured[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  static size_t configured[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
   size_t &cfg = configured[td ? 1 : 0][mode];
   if (smem > cfg) {
     FH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

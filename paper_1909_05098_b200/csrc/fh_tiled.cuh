@@ -34,6 +34,8 @@ struct TiledArgs {
   const S *tet_G, *hex_G;
   const S *tet_kf, *hex_kf;
   const uint8_t *tet_rank, *hex_rank;  // null: corner-unique (phase == corner)
+  const uint8_t *tet_phase, *hex_phase;  // colored mode: phase per slot
+  const uint8_t *tet_bnph, *hex_bnph;    // colored mode: phases per batch (index slot / B)
   const uint8_t *tet_region, *hex_region;
   int max_phase_tet, max_phase_hex;
   // smem carve-up (bytes) and ring depth
@@ -55,12 +57,13 @@ struct TiledArgs {
   unsigned long long step_no;
 };
 
-// bytes of one staged batch: conn16 [B][N] | G [6][B] | kf [B] | rank [B][N]
+// bytes of one staged batch: conn16 [B][N] | G [6][B] | kf [B] | rank [B][N] | phase [B]
 template <typename S>
-inline int StageBytes(int N, bool has_kf, bool has_rank) {
+inline int StageBytes(int N, bool has_kf, bool has_rank, bool has_phase = false) {
   int b = kBatch * N * 2 + 6 * kBatch * (int)sizeof(S);
   if (has_kf) b += kBatch * (int)sizeof(S);
   if (has_rank) b += kBatch * N;
+  if (has_phase) b += kBatch;
   return (b + 15) & ~15;
 }
 
@@ -69,7 +72,7 @@ void tiled_step(const TiledArgs<S> &g, int n_parts, bool td, int mode, size_t sm
 
 // accumulation mode of the step kernel (see fh_tiled.cu): 0 ranked phases,
 // 1 corner phases, 2 corner slots (the last two need corner-unique tiles)
-enum TileMode { kModeRanked = 0, kModeCornerPhase = 1, kModeCornerSlot = 2 };
+enum TileMode { kModeRanked = 0, kModeCornerPhase = 1, kModeCornerSlot = 2, kModeColored = 3 };
 
 // TI freeze: per-slot kbar (global-id connectivity conn4/conn8) and per-node
 // capacity / perfusion from Tin.

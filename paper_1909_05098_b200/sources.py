@@ -90,16 +90,22 @@ def static_nodal_power(sources, nodes, node_volumes) -> np.ndarray | None:
     return q
 
 
-def _boundary_faces(mesh):
-    """Faces (as sorted-corner tuples + corner lists) used by exactly one element."""
-    from .meshgen import KUHN_PATTERNS  # noqa: F401  (documentation of the tet corner order)
+def _boundary_faces(mesh, members):
+    """Faces with every corner in ``members`` that belong to exactly one element.
+
+    Only faces inside the node set can be its boundary faces, so the
+    multiplicity count runs on that (small) subset."""
     tet_faces = np.array([[0, 1, 2], [0, 1, 3], [0, 2, 3], [1, 2, 3]])
     hex_faces = np.array([[0, 1, 2, 3], [4, 5, 6, 7], [0, 1, 5, 4], [1, 2, 6, 5], [2, 3, 7, 6], [3, 0, 4, 7]])
     out = []
     for conn, faces in ((mesh.tets, tet_faces), (mesh.hexes, hex_faces)):
         if conn.size == 0:
             continue
-        f = conn[:, faces].reshape(-1, faces.shape[1])
+        cand = conn[members[conn].sum(axis=1) >= faces.shape[1]]
+        f = cand[:, faces].reshape(-1, faces.shape[1])
+        f = f[members[f].all(axis=1)]
+        if f.size == 0:
+            continue
         key = np.sort(f, axis=1)
         _, inv, cnt = np.unique(key, axis=0, return_inverse=True, return_counts=True)
         out.append(f[cnt[inv.ravel()] == 1])
@@ -118,10 +124,7 @@ def robin_lumps(mesh, spec: RobinSpec, exclude=None):
     members = np.zeros(mesh.n_nodes, bool)
     members[mesh.node_sets[spec.nodeset]] = True
     area = np.zeros(mesh.n_nodes)
-    for faces in _boundary_faces(mesh):
-        faces = faces[members[faces].all(axis=1)]
-        if faces.size == 0:
-            continue
+    for faces in _boundary_faces(mesh, members):
         p = mesh.nodes[faces]
         if faces.shape[1] == 3:
             a = 0.5 * np.linalg.norm(np.cross(p[:, 1] - p[:, 0], p[:, 2] - p[:, 0]), axis=1)

@@ -425,7 +425,9 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   st->hex_slot_elem.upload(P.hex_slot_elem, s);
   // accumulation mode (fh_tiled.cu): colour phases when the colouring fits,
   // else ranked phases; FH_TILE_MODE (0..3) overrides (tuning knob)
-  int mode = P.colored_ok ? kModeColored : kModeRanked;
+  // measured (scripts/sweep.py): corner phases win on corner-unique hex grids (cfg4),
+  // colour phases win on tets (cfg3, 1.45x over ranked)
+  int mode = P.corner_unique ? kModeCornerPhase : (P.colored_ok ? kModeColored : kModeRanked);
   if (const char *env = getenv("FH_TILE_MODE")) {
     const int m = atoi(env);
     if (m == kModeRanked || (m == kModeColored && P.colored_ok) ||

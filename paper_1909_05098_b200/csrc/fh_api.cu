@@ -368,6 +368,9 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   pin.hexes = mesh.hexes;
   pin.node_class = cls.data();
   pin.target_part_nodes = o.part_nodes > 0 ? o.part_nodes : (sizeof(S) == 4 ? 1536 : 768);
+  // small meshes: shrink the tiles so that at least ~2 CTAs per SM exist (latency-bound regime)
+  if (o.part_nodes <= 0 && V / pin.target_part_nodes < 2 * 148)
+    pin.target_part_nodes = (int)std::max<int64_t>(96, V / (2 * 148));
   pin.batch = kBatch;
   pin.n_domains = std::max(1, o.n_domains);
   pin.slab_axis = o.slab_axis;
@@ -434,15 +437,18 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
         ((m == kModeCornerPhase || m == kModeCornerSlot) && P.corner_unique))
       mode = m;
   }
-  if (mode == kModeRanked) {
-    st->tet_rank.upload(P.tet_rank, s);
-    st->hex_rank.upload(P.hex_rank, s);
-  }
+  // `mode` is the hex mode (kernel template); tets never are corner-unique and
+  // always use colour phases (or ranked phases if the colouring overflowed)
+  const int tet_mode = P.colored_ok ? kModeColored : kModeRanked;
+  if (mode == kModeRanked) st->hex_rank.upload(P.hex_rank, s);
+  if (tet_mode == kModeRanked) st->tet_rank.upload(P.tet_rank, s);
   if (mode == kModeColored) {
-    st->tet_phase.upload(P.tet_phase, s);
     st->hex_phase.upload(P.hex_phase, s);
-    st->tet_bnph.upload(P.tet_batch_nph, s);
     st->hex_bnph.upload(P.hex_batch_nph, s);
+  }
+  if (tet_mode == kModeColored) {
+    st->tet_phase.upload(P.tet_phase, s);
+    st->tet_bnph.upload(P.tet_batch_nph, s);
   }
   const int64_t nts = (int64_t)P.tet_slot_elem.size(), nhs = (int64_t)P.hex_slot_elem.size();
   st->tet_G.alloc(6 * nts);
@@ -566,7 +572,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.smem_acc = (int)al(sizeof(S) * (st->mode == kModeCornerSlot ? 8 : 1) * (size_t)std::max(1, P.max_part_free));
   int stage = 0;
   if (e->n_tet)
-    stage = std::max(stage, StageBytes<S>(4, st->tet_kf.p || !e->td, mode == kModeRanked, mode == kModeColored));
+    stage = std::max(stage, StageBytes<S>(4, st->tet_kf.p || !e->td, tet_mode == kModeRanked, tet_mode == kModeColored));
   if (e->n_hex)
     stage = std::max(stage, StageBytes<S>(8, st->hex_kf.p || !e->td, mode == kModeRanked, mode == kModeColored));
   g.stage_bytes = (int)al(stage);
@@ -1540,7 +1546,8 @@ int fh_plan_info(fh_plan *pl, int64_t *info, int32_t n_info) {
   const int64_t v[] = {pl->P.n_parts, pl->X.part_hi - pl->X.part_lo, pl->X.n_boundary, (int64_t)pl->X.peers.size(),
                        (int64_t)pl->X.send_nodes.size(), (int64_t)pl->X.recv_nodes.size(), pl->X.node_lo,
                        pl->X.node_hi, (int64_t)pl->P.corner_unique, pl->P.max_phase_tet, pl->P.max_phase_hex,
-                       (int64_t)(pl->P.tet_slot_elem.size() + pl->P.hex_slot_elem.size()), pl->P.max_local_nodes};
+                       (int64_t)(pl->P.tet_slot_elem.size() + pl->P.hex_slot_elem.size()), pl->P.max_local_nodes,
+                       (int64_t)pl->P.colored_ok, pl->P.max_colors, pl->P.max_nph_tet, pl->P.max_nph_hex};
   for (int q = 0; q < n_info && q < (int)(sizeof(v) / sizeof(v[0])); ++q) info[q] = v[q];
   FH_API_END
 }

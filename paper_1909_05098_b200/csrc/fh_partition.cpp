@@ -343,7 +343,7 @@ void build_partition(const PartitionInput &in, Partition &P) {
         for (int a = 0; a < N; ++a) {
           const int32_t loc = conn[(size_t)N * s + a] - n0;
           if (loc >= 0 && loc < nf) {
-            if (cornermask[loc] & (1u << a)) unique = false;
+            if ((cornermask[loc] & (1u << a)) && N == 8) unique = false;  // hexes only: tets use colours
             cornermask[loc] |= (uint16_t)(1u << a);
           }
         }

@@ -370,23 +370,22 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
           rk[q][a] = 0xff;
         }
         if (valid[q]) tet_loads<S, TD>(g, stage, sT, kc, g.tet_kf != nullptr, i, nd[q], c[q]);
-        if (MODE == kRanked && valid[q]) {
-          const StageLayout<S> L(4, g.tet_kf != nullptr, true);
-          const uint32_t w = reinterpret_cast<const uint32_t *>(stage + L.rank)[i];
-          rk[q][0] = w & 0xff; rk[q][1] = (w >> 8) & 0xff; rk[q][2] = (w >> 16) & 0xff; rk[q][3] = w >> 24;
-        }
-        if (MODE == kColored && valid[q]) {
+        // tets are never corner-unique: colour phases (phase byte per slot) or,
+        // if the colouring overflowed, ranked phases (rank byte per corner)
+        if (valid[q] && g.tet_phase) {
           const StageLayout<S> L(4, g.tet_kf != nullptr, false);
           const uint8_t ph = stage[L.phase + i];
 #pragma unroll
           for (int a = 0; a < 4; ++a) rk[q][a] = ph;
+        } else if (valid[q]) {
+          const StageLayout<S> L(4, g.tet_kf != nullptr, true);
+          const uint32_t w = reinterpret_cast<const uint32_t *>(stage + L.rank)[i];
+          rk[q][0] = w & 0xff; rk[q][1] = (w >> 8) & 0xff; rk[q][2] = (w >> 16) & 0xff; rk[q][3] = w >> 24;
         }
       }
-      if (MODE == kColored)  // every corner of a slot is added in its colour's phase
-        accumulate<S, 4, kRanked>(acc, nd, c, nfree, valid, rk,
-                                  g.tet_bnph[(g.part_tet_start[p] + b * kBatch) / kBatch]);
-      else
-        accumulate<S, 4, MODE>(acc, nd, c, nfree, valid, rk, g.max_phase_tet);
+      accumulate<S, 4, kRanked>(acc, nd, c, nfree, valid, rk,
+                                g.tet_phase ? (int)g.tet_bnph[(g.part_tet_start[p] + b * kBatch) / kBatch]
+                                            : g.max_phase_tet);
     } else {
       uint16_t nd[kSPT][8];
       S c[kSPT][8];

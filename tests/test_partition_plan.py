@@ -70,12 +70,18 @@ def test_partition_matches_restatement_bitwise(kind, div, ndom, target, slab):
     assert np.array_equal(again.new_to_old, plan.new_to_old)
 
 
-def test_structured_hex_is_corner_unique_and_tets_are_ranked():
+def test_structured_hex_is_corner_unique_and_tets_are_coloured():
     hexm = fh.generate_cube_mesh("hex", 8, 0.1)
     assert Plan(hexm, MAT, part_nodes=100).info["corner_unique"] == 1
-    tetm = fh.generate_cube_mesh("tet", 6, 0.1)
-    info = Plan(tetm, MAT, part_nodes=100).info
-    assert info["corner_unique"] == 0 and 1 <= info["max_phase_tet"] <= 32
+    tetm = fh.generate_cube_mesh("tet", 20, 0.1)
+    info = Plan(tetm, MAT, part_nodes=1536).info
+    assert 1 <= info["max_phase_tet"] <= 32  # ranked fallback stays within the byte encoding
+    # Kuhn tets: every interior node touches 24 tets -> >= 24 colours; with
+    # production-size tiles a 256-slot batch spans only a few colours
+    assert info["colored_ok"] == 1 and 24 <= info["max_colors"] <= 64
+    assert info["max_nph_tet"] <= 8
+    hexm = fh.jittered_cube_mesh("hex", 6, 0.1, 0.1, seed=1)
+    assert Plan(hexm, MAT, part_nodes=100).info["max_colors"] <= 16  # greedy: about 8-12 colours
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])

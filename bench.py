@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="fast", choices=["fast", "reference"])
-    ap.add_argument("--config", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--config", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--precision", type=int, default=0)
     ap.add_argument("--divisions", type=int, default=0, help="override mesh divisions (testing)")
     ap.add_argument("--part-nodes", type=int, default=0)
@@ -66,7 +66,7 @@ def make_problem(name, divisions=0, precision=0):
     fn = getattr(configs, name)
     kw = {}
     if divisions:
-        kw["divisions"] = divisions
+        kw["scale" if name == "cfg5" else "divisions"] = divisions
     if precision and name in ("cfg2", "cfg3"):
         kw["precision"] = precision
     prob = fn(**kw)
@@ -143,9 +143,9 @@ def cpu_oracle_rate(name, divisions, steps, threads=None, per_step=False):
         robin = robin_lumps(mesh, prob.robin[0], exclude=rb.dirichlet_nodes)
     if threads:
         orc.set_threads(threads)
-    ora = orc.OracleModel(mesh, prob.material, dirichlet=(rb.dirichlet_nodes, rb.dirichlet_values),
+    ora = orc.OracleModel(mesh, prob.materials or prob.material, dirichlet=(rb.dirichlet_nodes, rb.dirichlet_values),
                           sources=[s.as_dict() for s in prob.sources], robin=robin, kfactor=prob.kfactor,
-                          td_mode=prob.td_mode)
+                          elem_region=prob.element_region, td_mode=prob.td_mode)
     ora.initial_state(37.0)
     dt = 0.9 * ora.critical_dt(np.full(mesh.n_nodes, 37.0))
     ora.step(dt, 1)  # warm-up
@@ -166,13 +166,14 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    div = args.cpu_sample_div or {"cfg4": 96, "cfg3": 40, "cfg1": 20, "cfg2": 20}[args.config]
+    div = args.cpu_sample_div or {"cfg4": 96, "cfg3": 40, "cfg1": 20, "cfg2": 20, "cfg5": 4}[args.config]
     # warm-up steps inside cpu_oracle_rate: 1 + W, then K timed steps
     times, elem, threads = cpu_oracle_rate(args.config, div, args.warmup + args.steps, per_step=True)
     per_step = times[args.warmup:]
     tot = sum(per_step)
     value = elem * len(per_step) / tot
-    sample = (f"{args.config}-family mesh at {div}^3 cells ({elem} elements; the full workload is sampled "
+    size = f"grid / {div}" if args.config == "cfg5" else f"{div}^3 cells"
+    sample = (f"{args.config}-family mesh at {size} ({elem} elements; the full workload is sampled "
               f"per element), one oracle step (oracle/fh_oracle.c, reference op order, OpenMP) per bench step")
     line = {
         "impl": "reference", "metric": "element-steps/sec", "value": value, "unit": "element-steps/s",
@@ -293,11 +294,12 @@ def main():
             traffic = json.load(f).get(args.config)
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1:
-        div = args.cpu_sample_div or {"cfg4": 96, "cfg3": 40, "cfg1": 20, "cfg2": 20}[args.config]
+        div = args.cpu_sample_div or {"cfg4": 96, "cfg3": 40, "cfg1": 20, "cfg2": 20, "cfg5": 4}[args.config]
         rate, el, elem, threads = cpu_oracle_rate(args.config, div, 3)
         cpu = {"value": rate, "unit": "element-steps/s", "cores": threads, "kind": "port",
-               "sample": f"oracle (fh_oracle.c, fp64, reference op order) on the {args.config} family at {div}^3 "
-                         f"cells ({elem} elements), 3 steps after 1 warm-up"}
+               "sample": f"oracle (fh_oracle.c, fp64, reference op order) on the {args.config} family at "
+                         f"{'grid / ' + str(div) if args.config == 'cfg5' else str(div) + '^3 cells'} "
+                         f"({elem} elements), 3 steps after 1 warm-up"}
     line = {
         "metric": "element-steps/sec", "value": value, "unit": "element-steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,

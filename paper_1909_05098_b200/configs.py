@@ -14,7 +14,7 @@ import numpy as np
 from .material import TissueMaterial, linear_law, make_constant
 from .meshgen import generate_cube_mesh, jittered_cube_mesh
 from .solver import BoundarySpec
-from .sources import GaussianSource, RobinSpec
+from .sources import GaussianSource, RFSource, RobinSpec
 
 FACES = ("x0", "x1", "y0", "y1", "z0", "z1")
 PERFUSION_SLOPE = 0.002  # 1/K, open parameter
@@ -34,10 +34,15 @@ class Problem:
     kfactor: np.ndarray | None = None
     auto_dt_safety: float = 0.9
     notes: dict = field(default_factory=dict)
+    materials: list | None = None
+    element_region: np.ndarray | None = None
 
     def engine_kwargs(self):
-        return dict(td_mode=self.td_mode, precision=self.precision, sources=self.sources, robin=self.robin,
-                    kfactor=self.kfactor)
+        kw = dict(td_mode=self.td_mode, precision=self.precision, sources=self.sources, robin=self.robin,
+                  kfactor=self.kfactor)
+        if self.materials is not None:
+            kw.update(materials=self.materials, element_region=self.element_region)
+        return kw
 
 
 def pennes_constant() -> TissueMaterial:
@@ -78,6 +83,40 @@ def cfg3(divisions: int = 100, precision: int = 32, seed: int = 3) -> Problem:
     bnd = BoundarySpec(dirichlet=tuple((f, 37.0) for f in FACES if f != "z1"))
     return Problem("cfg3", mesh, pennes_td(), bnd, steps=500, precision=precision, td_mode=True, sources=srcs,
                    robin=(RobinSpec("z1", 10.0, 25.0),))
+
+
+def cfg5(scale: int = 1, seed: int = 5) -> Problem:
+    """Organ-like domain: ellipsoid (0.15 x 0.10 x 0.08 m) voxel-masked from a
+    512 x 384 x 320 grid (h = 0.3/512 m; ``scale`` divides the grid for tests),
+    10 % of boundary voxels split into tets, tumour sphere r = 15 mm (k 0.55,
+    w_b 0.2e-3 1/s) in healthy tissue (k 0.5, w_b 0.6e-3 1/s), cfg2 laws, RF
+    source at the tumour centre (P = 5 W, capped 1e8 W/m^3), Dirichlet 37 C on
+    the organ surface (open parameters)."""
+    from .meshgen import voxel_ellipsoid_mesh
+
+    dims = (512 // scale, 384 // scale, 320 // scale)
+    h = 0.3 / 512 * scale
+    mesh, centre = voxel_ellipsoid_mesh(dims, h, seed=seed)
+    rng = np.random.default_rng(seed + 1)
+    # tumour centre: seeded, at least r = 15 mm inside the ellipsoid
+    inner = np.array([0.15, 0.10, 0.08]) - 0.02
+    while True:
+        off = rng.uniform(-1.0, 1.0, 3) * inner
+        if ((off / inner) ** 2).sum() <= 1.0:
+            break
+    tumour = centre + off
+    conn = [mesh.tets, mesh.hexes]
+    cent = np.concatenate([mesh.nodes[c].mean(axis=1) for c in conn if c.size])
+    region = (np.linalg.norm(cent - tumour, axis=1) < 0.015).astype(np.int32)
+    healthy = pennes_td(k0=0.5, wb0=0.6e-3 * 1050.0)
+    tumour_mat = pennes_td(k0=0.55, wb0=0.2e-3 * 1050.0)
+    src = RFSource(power=5.0, tip=tuple(tumour), cap=1.0e8)
+    bnd = BoundarySpec(dirichlet=(("surface", 37.0),))
+    prob = Problem("cfg5", mesh, healthy, bnd, steps=500, precision=32, td_mode=True, sources=(src,),
+                   notes={"tumour_centre": tumour.tolist(), "regions": region})
+    prob.materials = [healthy, tumour_mat]
+    prob.element_region = region
+    return prob
 
 
 def cfg4(divisions: int = 256, seed: int = 4) -> Problem:

@@ -99,6 +99,72 @@ def generate_cube_mesh(kind, divisions: int, size: float) -> Mesh:
     return Mesh(nodes=nodes, tets=tets, hexes=hexes, node_sets=sets)
 
 
+def voxel_ellipsoid_mesh(dims=(512, 384, 320), h: float = 0.3 / 512, semi=(0.15, 0.10, 0.08),
+                         split_fraction: float = 0.1, seed: int = 5):
+    """Config-5 mesh: voxels of a (nx, ny, nz) grid of spacing h whose centre
+    lies inside the ellipsoid (semi-axes ``semi``, centred in the grid) become
+    hex8 elements; a seeded ``split_fraction`` of the boundary voxels (active
+    voxels with an inactive face neighbour) are split into 6 Kuhn tets.
+    Node set ``surface``: nodes on faces shared with an inactive voxel.
+    Returns (mesh, centre)."""
+    nx, ny, nz = (int(d) for d in dims)
+    centre = np.array([nx * h / 2.0, ny * h / 2.0, nz * h / 2.0])
+    xs = (((np.arange(nx) + 0.5) * h - centre[0]) / semi[0]) ** 2
+    ys = (((np.arange(ny) + 0.5) * h - centre[1]) / semi[1]) ** 2
+    zs = (((np.arange(nz) + 0.5) * h - centre[2]) / semi[2]) ** 2
+    active = (zs[:, None, None] + ys[None, :, None] + xs[None, None, :]) <= 1.0  # [k, j, i]
+    pad = np.pad(active, 1)
+    exposed = []  # per direction: active cells whose neighbour is inactive
+    for axis in range(3):
+        for step in (-1, 1):
+            nb = np.roll(pad, -step, axis=axis)[1:-1, 1:-1, 1:-1]
+            exposed.append(active & ~nb)
+    boundary = np.logical_or.reduce(exposed)
+    kb, jb, ib = np.nonzero(boundary)
+    rng = np.random.default_rng(seed)
+    n_split = int(round(split_fraction * kb.size))
+    pick = np.sort(rng.choice(kb.size, size=n_split, replace=False))
+    split = np.zeros_like(active)
+    split[kb[pick], jb[pick], ib[pick]] = True
+    # grid points used by active voxels -> compact node ids (x fastest)
+    gx, gy = nx + 1, ny + 1
+    used = np.zeros((nz + 1, ny + 1, nx + 1), dtype=bool)
+    for dk in (0, 1):
+        for dj in (0, 1):
+            for di in (0, 1):
+                used[dk:dk + nz, dj:dj + ny, di:di + nx] |= active
+    flat_used = used.ravel()
+    node_id = np.cumsum(flat_used, dtype=np.int64) - 1
+    gidx = np.nonzero(flat_used)[0]
+    k_, rem = np.divmod(gidx, gx * gy)
+    j_, i_ = np.divmod(rem, gx)
+    nodes = np.stack([i_ * h, j_ * h, k_ * h], axis=1).astype(np.float64)
+    stride = np.array([1, gx, gx * gy], dtype=np.int64)
+
+    def cells(mask):
+        k, j, i = np.nonzero(mask)
+        return i + gx * (j + gy * k)
+
+    hex_base = cells(active & ~split)
+    hexes = node_id[hex_base[:, None] + (HEX_CORNER_OFFSETS @ stride)[None]]
+    tet_base = cells(split)
+    tets = node_id[(tet_base[:, None, None] + (KUHN_PATTERNS @ stride)[None])].reshape(-1, 4)
+    surf = np.zeros(flat_used.size, dtype=bool)
+    faces = {(0, -1): [0, 3, 4, 7], (0, 1): [1, 2, 5, 6], (1, -1): [0, 1, 4, 5], (1, 1): [2, 3, 6, 7],
+             (2, -1): [0, 1, 2, 3], (2, 1): [4, 5, 6, 7]}
+    q = 0
+    for axis in range(3):
+        for step in (-1, 1):
+            base = cells(exposed[q])
+            q += 1
+            axis_map = {0: 2, 1: 1, 2: 0}  # exposed[] axes are (k, j, i) -> (z, y, x)
+            corners = faces[(axis_map[axis], step)]
+            for c in corners:
+                surf[base + HEX_CORNER_OFFSETS[c] @ stride] = True
+    sets = {"surface": node_id[np.nonzero(surf)[0]]}
+    return Mesh(nodes=nodes, tets=tets, hexes=hexes, node_sets=sets), centre
+
+
 def jittered_cube_mesh(kind, divisions: int, size: float, jitter: float = 0.2,
                        seed: int = 0) -> Mesh:
     """Config-3 mesh: cube numbering, interior nodes moved by U(-jitter*h, +jitter*h)

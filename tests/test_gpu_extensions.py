@@ -118,3 +118,21 @@ def test_td_perfusion_fixed_point_bitwise():
         for _ in range(10):
             eng.step(st, 1.0)
         assert np.all(st.temperatures == 37.0), assembly
+
+
+@pytest.mark.parametrize("assembly,prec,tol", [("exact", 64, 0.0), ("tiled", 64, 1e-10), ("tiled", 32, 1e-4)])
+def test_cfg5_family_mixed_voxel_regions(assembly, prec, tol):
+    """Voxel ellipsoid (hexes + split boundary tets), two regions, RF source."""
+    prob = configs.cfg5(scale=16)
+    assert prob.mesh.tets.shape[0] > 0 and prob.element_region.sum() > 0
+    eng = fh.ExplicitEngine(prob.mesh, prob.material, prob.boundary, assembly=assembly, precision=prec,
+                            part_nodes=400, **{k: v for k, v in prob.engine_kwargs().items() if k != "precision"})
+    dt = 0.9 * eng.critical_dt(37.0)
+    res = eng.run(37.0, steps=40, dt=dt)
+    ora = oracle_of(eng, prob.sources, materials=prob.materials, element_region=prob.element_region)
+    T_ref, _ = ora.run(37.0, 40, dt)
+    assert T_ref.max() > 37.01
+    if tol == 0.0:
+        assert np.array_equal(res.state.temperatures, T_ref)
+    else:
+        assert rel(res.state.temperatures, T_ref) <= tol

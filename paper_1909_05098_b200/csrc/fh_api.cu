@@ -430,10 +430,11 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   // else ranked phases; FH_TILE_MODE (0..3) overrides (tuning knob)
   // measured (scripts/sweep.py): corner phases win on corner-unique hex grids (cfg4),
   // colour phases win on tets (cfg3, 1.45x over ranked)
-  int mode = P.corner_unique ? kModeCornerPhase : (P.colored_ok ? kModeColored : kModeRanked);
+  const bool hex_colour_ok = P.colored_ok && P.hex_colored;
+  int mode = P.corner_unique ? kModeCornerPhase : (hex_colour_ok ? kModeColored : kModeRanked);
   if (const char *env = getenv("FH_TILE_MODE")) {
     const int m = atoi(env);
-    if (m == kModeRanked || (m == kModeColored && P.colored_ok) ||
+    if (m == kModeRanked || (m == kModeColored && hex_colour_ok) ||
         ((m == kModeCornerPhase || m == kModeCornerSlot) && P.corner_unique))
       mode = m;
   }

@@ -151,6 +151,7 @@ struct Partition {
   // colouring: slots of one colour share no updated node; slots are sorted by
   // colour inside each tile, phase = colour index inside the batch
   bool colored_ok = false;
+  bool hex_colored = false;  // hex slots colour-sorted (only when hexes are not corner-unique)
   int max_colors = 0, max_nph_tet = 0, max_nph_hex = 0;
   std::vector<uint8_t> tet_color, hex_color, tet_phase, hex_phase;
   std::vector<uint8_t> tet_batch_nph, hex_batch_nph;  // phases per batch (index = slot / B)

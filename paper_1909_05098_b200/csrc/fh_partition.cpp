@@ -241,13 +241,44 @@ void build_partition(const PartitionInput &in, Partition &P) {
       for (size_t q = 0; q < v.size(); ++q) v[q] = ct[q].second;
       return ct;
     };
+    // Hexes that are corner-unique inside every tile use corner phases and
+    // keep the min-corner order (neighbouring threads touch neighbouring
+    // nodes); a colour sort would interleave them and double the shared-memory
+    // wavefronts (measured: 0.426 -> 0.48 ms/step on cfg4).
+    bool hex_unique = true;
+    {
+      std::vector<uint8_t> mask(P.max_part_nodes, 0);
+      for (int p = 0; p < P.n_parts && hex_unique; ++p) {
+        const int64_t n0 = P.part_node_start[p], nf = P.part_n_free[p];
+        for (int32_t e : hex_pp[p]) {
+          const int64_t *c = in.hexes + 8 * ((int64_t)e - in.n_tet);
+          for (int a = 0; a < 8; ++a) {
+            const int64_t loc = P.new_of_old[c[a]] - n0;
+            if (loc < 0 || loc >= nf) continue;
+            if (mask[loc] & (1u << a)) hex_unique = false;
+            mask[loc] |= (uint8_t)(1u << a);
+          }
+        }
+        for (int32_t e : hex_pp[p]) {
+          const int64_t *c = in.hexes + 8 * ((int64_t)e - in.n_tet);
+          for (int a = 0; a < 8; ++a) {
+            const int64_t loc = P.new_of_old[c[a]] - n0;
+            if (loc >= 0 && loc < nf) mask[loc] = 0;
+          }
+        }
+      }
+    }
+    P.hex_colored = !hex_unique;
     P.tet_color.clear();
     P.hex_color.clear();
     tet_color_pp.assign(P.n_parts, {});
     hex_color_pp.assign(P.n_parts, {});
     for (int p = 0; p < P.n_parts; ++p) {
       for (auto &x : colour_part(tet_pp[p], 4, p)) tet_color_pp[p].push_back((uint8_t)x.first);
-      for (auto &x : colour_part(hex_pp[p], 8, p)) hex_color_pp[p].push_back((uint8_t)x.first);
+      if (P.hex_colored)
+        for (auto &x : colour_part(hex_pp[p], 8, p)) hex_color_pp[p].push_back((uint8_t)x.first);
+      else
+        hex_color_pp[p].assign(hex_pp[p].size(), 0);
     }
   }
   P.part_tet_start.assign(P.n_parts + 1, 0);

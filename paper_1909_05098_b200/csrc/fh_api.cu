@@ -91,14 +91,16 @@ __global__ void k_to_old(const S *__restrict__ src_new, const int64_t *__restric
 }
 
 template <typename S>
-__global__ void k_xyz_to_new(const double *__restrict__ xyz, const int64_t *__restrict__ old_of_new, int64_t V,
-                             S *__restrict__ out) {
+__global__ void k_xyzv_to_new(const double *__restrict__ xyz, const int64_t *__restrict__ old_of_new,
+                              const S *__restrict__ vol_new, int64_t V, S *__restrict__ out) {
+  // packed (x, y, z, v) per node, new numbering: one vector load in the step kernel
   const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (n >= V) return;
   const int64_t o = old_of_new[n];
-  out[3 * n] = (S)xyz[3 * o];
-  out[3 * n + 1] = (S)xyz[3 * o + 1];
-  out[3 * n + 2] = (S)xyz[3 * o + 2];
+  out[4 * n] = (S)xyz[3 * o];
+  out[4 * n + 1] = (S)xyz[3 * o + 1];
+  out[4 * n + 2] = (S)xyz[3 * o + 2];
+  out[4 * n + 3] = vol_new[n];
 }
 
 template <typename S>
@@ -434,7 +436,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   int mode = P.corner_unique ? kModeCornerPhase : (hex_colour_ok ? kModeColored : kModeRanked);
   if (const char *env = getenv("FH_TILE_MODE")) {
     const int m = atoi(env);
-    if (m == kModeRanked || (m == kModeColored && hex_colour_ok) ||
+    if (m == kModeRanked || m == kModeSharedAtomic || (m == kModeColored && hex_colour_ok) ||
         ((m == kModeCornerPhase || m == kModeCornerSlot) && P.corner_unique))
       mode = m;
   }
@@ -505,10 +507,9 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     }
   }
   if (!e->sources.empty()) {
-    std::vector<S> x(3 * V);
-    for (int64_t n = 0; n < V; ++n)
-      for (int d = 0; d < 3; ++d) x[3 * n + d] = (S)mesh.coords[3 * P.old_of_new[n] + d];
-    st->xyz.upload(x, s);
+    st->xyz.alloc(4 * V);
+    k_xyzv_to_new<S><<<nblk(V), kBlk, 0, s>>>(e->xyz.p, e->old_of_new.p, st->vol.p, V, st->xyz.p);
+    FH_CUDA(cudaGetLastError());
   }
   if (!e->robin_nodes.empty()) {
     // compact robin arrays ordered like the renumbered robin nodes
@@ -555,7 +556,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.cap_frozen = st->cap.p;
   g.kb_frozen = st->kb.p;
   g.q_ext = st->q_ext.p;
-  g.xyz = st->xyz.p;
+  g.xyzv = st->xyz.p;
   g.node_region = st->node_region.p;
   g.robin_hA = st->robin_hA.p;
   g.robin_hAT = st->robin_hAT.p;
@@ -570,7 +571,8 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.n_stages = 2;  // measured best on cfg4 (scripts/sweep.py)
   if (const char *env = getenv("FH_TILE_STAGES")) g.n_stages = std::min(kMaxStages, std::max(1, atoi(env)));
   g.smem_T = (int)al(2 * sizeof(S) * (size_t)std::max(1, P.max_local_nodes));
-  g.smem_acc = (int)al(sizeof(S) * (st->mode == kModeCornerSlot ? 8 : 1) * (size_t)std::max(1, P.max_part_free));
+  // +1: the trash slot of the corner-phase accumulation
+  g.smem_acc = (int)al(sizeof(S) * (st->mode == kModeCornerSlot ? 8 : 1) * ((size_t)std::max(1, P.max_part_free) + 1));
   int stage = 0;
   if (e->n_tet)
     stage = std::max(stage, StageBytes<S>(4, st->tet_kf.p || !e->td, tet_mode == kModeRanked, tet_mode == kModeColored));
@@ -1116,10 +1118,10 @@ int fh_set_sources(fh_engine *e, const fh_source *sources, int32_t n) {
     auto setup = [&](auto &st) {
       using S = std::remove_reference_t<decltype(*st.T[0].p)>;
       if (n > 0 && !st.xyz.p) {
-        st.xyz.alloc(3 * e->V);
-        k_xyz_to_new<S><<<nblk(e->V), kBlk, 0, e->stream>>>(e->xyz.p, e->old_of_new.p, e->V, st.xyz.p);
+        st.xyz.alloc(4 * e->V);
+        k_xyzv_to_new<S><<<nblk(e->V), kBlk, 0, e->stream>>>(e->xyz.p, e->old_of_new.p, st.vol.p, e->V, st.xyz.p);
         FH_CUDA(cudaGetLastError());
-        st.args.xyz = st.xyz.p;
+        st.args.xyzv = st.xyz.p;
       }
       st.args.n_src = n;
     };

@@ -32,6 +32,10 @@ constexpr unsigned long long kNone = ~0ull;
 #define FH_MIN_BLOCKS_F32 4
 #endif
 constexpr int kMinBlocksF32 = FH_MIN_BLOCKS_F32;
+// corner phases: predicated accumulation (0) or unpredicated into a trash slot (1)
+#ifndef FH_TRASH_SLOT
+#define FH_TRASH_SLOT 0
+#endif
 
 // (T, k(T)) of a tile-local node, staged once per tile in shared memory
 template <typename S>
@@ -98,6 +102,17 @@ __device__ __forceinline__ S kbar_from(const Curve<S> &kc, const S *Tn, int n, S
 
 __device__ __forceinline__ float fast_div(float a, float b) { return __fdividef(a, b); }
 __device__ __forceinline__ double fast_div(double a, double b) { return a / b; }
+__device__ __forceinline__ void load_xyzv(const float *p, float &x, float &y, float &z, float &v) {
+  const float4 a = __ldg(reinterpret_cast<const float4 *>(p));
+  x = a.x; y = a.y; z = a.z; v = a.w;
+}
+__device__ __forceinline__ void load_xyzv(const double *p, double &x, double &y, double &z, double &v) {
+  const double2 a = __ldg(reinterpret_cast<const double2 *>(p)), b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
+  x = a.x; y = a.y; z = b.x; v = b.y;
+}
+// fp32: hardware ex2 (2 ulp, well inside the 1e-4 fp32 tolerance); fp64: libm
+__device__ __forceinline__ float fast_exp(float x) { return __expf(x); }
+__device__ __forceinline__ double fast_exp(double x) { return exp(x); }
 
 // F - kb T + qb + qm + q_ext with C, kb from the material laws (TD) or the
 // frozen arrays (TI); returns the rate, writes the capacity
@@ -124,7 +139,7 @@ __device__ __forceinline__ S sources_at(const TiledArgs<S> &g, const S *xyz) {
     const S dx = x - s.cx, dy = y - s.cy, dz = z - s.cz;
     const S r2 = (dx * dx + dy * dy) + dz * dz;
     if (s.kind == FH_SOURCE_GAUSSIAN)
-      q += s.amp * exp(-r2 * s.inv2s2);
+      q += s.amp * fast_exp(-r2 * s.inv2s2);
     else
       q += r2 > S(0) ? min(s.cap, s.inv4pi_amp / r2) : s.cap;
   }
@@ -245,7 +260,9 @@ __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned 
 //   kColored     slots sorted by colour (no two slots of a colour share an
 //                updated node): phase = colour index inside the batch, so a
 //                batch needs as many barriers as it holds colours (1-2)
-enum { kRanked = 0, kCornerPhase = 1, kCornerSlot = 2, kColored = 3 };
+//   kSharedAtomic  red.shared.add per corner, one barrier per batch: fastest
+//                but the summation order is not fixed (tolerance-only, opt-in)
+enum { kRanked = 0, kCornerPhase = 1, kCornerSlot = 2, kColored = 3, kSharedAtomic = 4 };
 
 template <typename S, int N, int MODE>
 __device__ __forceinline__ void accumulate(S *acc, const uint16_t (&nd)[kSPT][N], const S (&c)[kSPT][N], int nfree,
@@ -262,12 +279,34 @@ __device__ __forceinline__ void accumulate(S *acc, const uint16_t (&nd)[kSPT][N]
       for (int a = 0; a < N; ++a)
         if (loc[q][a] >= 0) acc[a * nfree + loc[q][a]] = -c[q][a];
     __syncthreads();  // stage buffer fully consumed before it is refilled
-  } else if (MODE == kCornerPhase) {
+  } else if (MODE == kSharedAtomic) {
+    // non-deterministic (summation order varies run to run; tolerance-only)
+#pragma unroll
+    for (int q = 0; q < kSPT; ++q)
+#pragma unroll
+      for (int a = 0; a < N; ++a)
+        if (loc[q][a] >= 0) atomicAdd(&acc[loc[q][a]], -c[q][a]);
+    __syncthreads();  // stage buffer fully consumed before it is refilled
+  } else if (MODE == kCornerPhase && !FH_TRASH_SLOT) {
 #pragma unroll
     for (int a = 0; a < N; ++a) {
 #pragma unroll
       for (int q = 0; q < kSPT; ++q)
         if (loc[q][a] >= 0) acc[loc[q][a]] -= c[q][a];
+      __syncthreads();
+    }
+  } else if (MODE == kCornerPhase) {
+    // corners the tile does not update (halo, Dirichlet, padding slots) add
+    // into the trash slot acc[nfree] (never read): no predicates per phase
+    int tl[kSPT][N];
+#pragma unroll
+    for (int q = 0; q < kSPT; ++q)
+#pragma unroll
+      for (int a = 0; a < N; ++a) tl[q][a] = valid[q] ? min((int)nd[q][a], nfree) : nfree;
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+#pragma unroll
+      for (int q = 0; q < kSPT; ++q) acc[tl[q][a]] -= c[q][a];
       __syncthreads();
     }
   } else {
@@ -281,7 +320,8 @@ __device__ __forceinline__ void accumulate(S *acc, const uint16_t (&nd)[kSPT][N]
     }
   }
 }
-template <typename S, bool TD, int MODE>
+// KINDS: 0 hex-only, 1 tet-only, 2 mixed mesh (the absent kind's path is compiled out)
+template <typename S, bool TD, int MODE, int KINDS>
 __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 : 2) k_tiled_step(const __grid_constant__ TiledArgs<S> g) {
   extern __shared__ __align__(128) unsigned char smem[];
   TK<S> *sT = reinterpret_cast<TK<S> *>(smem);
@@ -348,7 +388,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
   for (int j = 0; j < nb; ++j) {
     unsigned char *stage = ring + st * g.stage_bytes;
     mbar_wait(&bars[st], parity);
-    const bool tet = j < nbt;
+    const bool tet = KINDS == 1 || (KINDS == 2 && j < nbt);
     const int b = tet ? j : j - nbt;
     const int cnt = tet ? g.part_tet_count[p] : g.part_hex_count[p];
     bool valid[kSPT];
@@ -447,14 +487,13 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
       const int loc = base + u * kTileThreads;
       const bool ok = loc < nfree;
       const int n = n0 + (ok ? loc : 0);
-      v[u] = __ldg(g.vol + n);
       q[u] = g.q_ext ? __ldg(g.q_ext + n) : S(0);
       cf[u] = TD ? S(0) : __ldg(g.cap_frozen + n);
       kf[u] = (!TD && g.kb_frozen) ? __ldg(g.kb_frozen + n) : S(0);
-      if (g.n_src) {
-        px[u] = __ldg(g.xyz + 3 * (size_t)n);
-        py[u] = __ldg(g.xyz + 3 * (size_t)n + 1);
-        pz[u] = __ldg(g.xyz + 3 * (size_t)n + 2);
+      if (g.n_src) {  // packed (x, y, z, v): one vector load per node
+        load_xyzv(g.xyzv + 4 * (size_t)n, px[u], py[u], pz[u], v[u]);
+      } else {
+        v[u] = __ldg(g.vol + n);
       }
     }
 #pragma unroll
@@ -499,15 +538,23 @@ template <typename S>
 void tiled_step(const TiledArgs<S> &g, int n_parts, bool td, int mode_sel, size_t smem, cudaStream_t s) {
   if (n_parts <= 0) return;
   using K = void (*)(TiledArgs<S>);
-  static const K table[2][4] = {
-      {k_tiled_step<S, false, kRanked>, k_tiled_step<S, false, kCornerPhase>, k_tiled_step<S, false, kCornerSlot>,
-       k_tiled_step<S, false, kColored>},
-      {k_tiled_step<S, true, kRanked>, k_tiled_step<S, true, kCornerPhase>, k_tiled_step<S, true, kCornerSlot>,
-       k_tiled_step<S, true, kColored>}};
-  const int mode = mode_sel < 0 || mode_sel > 3 ? 0 : mode_sel;
-  const K kern = table[td ? 1 : 0][mode];
-  static size_t configured[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
-  size_t &cfg = configured[td ? 1 : 0][mode];
+  // [td][kinds][hex mode]; tet-only meshes ignore the hex mode
+#define FH_MODES(TDV, KV)                                                                          \
+  {k_tiled_step<S, TDV, kRanked, KV>, k_tiled_step<S, TDV, kCornerPhase, KV>,                       \
+   k_tiled_step<S, TDV, kCornerSlot, KV>, k_tiled_step<S, TDV, kColored, KV>,                       \
+   k_tiled_step<S, TDV, kSharedAtomic, KV>}
+#define FH_TETONLY(TDV)                                                                            \
+  {k_tiled_step<S, TDV, kRanked, 1>, k_tiled_step<S, TDV, kRanked, 1>, k_tiled_step<S, TDV, kRanked, 1>, \
+   k_tiled_step<S, TDV, kRanked, 1>, k_tiled_step<S, TDV, kRanked, 1>}
+  static const K table[2][3][5] = {{FH_MODES(false, 0), FH_TETONLY(false), FH_MODES(false, 2)},
+                                   {FH_MODES(true, 0), FH_TETONLY(true), FH_MODES(true, 2)}};
+#undef FH_MODES
+#undef FH_TETONLY
+  const int mode = mode_sel < 0 || mode_sel > 4 ? 0 : mode_sel;
+  const int kinds = (g.part_tet_start && g.tet_conn16 && g.hex_conn16) ? 2 : (g.hex_conn16 ? 0 : 1);
+  const K kern = table[td ? 1 : 0][kinds][mode];
+  static size_t configured[2][3][5] = {};
+  size_t &cfg = configured[td ? 1 : 0][kinds][mode];
   if (smem > cfg) {
     FH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cfg = smem;

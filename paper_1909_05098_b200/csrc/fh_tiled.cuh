@@ -46,7 +46,7 @@ struct TiledArgs {
   const S *vol;
   const S *cap_frozen, *kb_frozen;  // TI
   const S *q_ext;                   // heat loads + static sources (W) or null
-  const S *xyz;                     // 3 per node, for time-dependent sources
+  const S *xyzv;                    // (x, y, z, v) per node, for time-dependent sources
   const uint8_t *node_region;
   const S *robin_hA, *robin_hAT;
   MatSet<S> mats;
@@ -72,7 +72,7 @@ void tiled_step(const TiledArgs<S> &g, int n_parts, bool td, int mode, size_t sm
 
 // accumulation mode of the step kernel (see fh_tiled.cu): 0 ranked phases,
 // 1 corner phases, 2 corner slots (the last two need corner-unique tiles)
-enum TileMode { kModeRanked = 0, kModeCornerPhase = 1, kModeCornerSlot = 2, kModeColored = 3 };
+enum TileMode { kModeRanked = 0, kModeCornerPhase = 1, kModeCornerSlot = 2, kModeColored = 3, kModeSharedAtomic = 4 };
 
 // TI freeze: per-slot kbar (global-id connectivity conn4/conn8) and per-node
 // capacity / perfusion from Tin.

@@ -433,11 +433,14 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   // measured (scripts/sweep.py): corner phases win on corner-unique hex grids (cfg4),
   // colour phases win on tets (cfg3, 1.45x over ranked)
   const bool hex_colour_ok = P.colored_ok && P.hex_colored;
-  int mode = P.corner_unique ? kModeCornerPhase : (hex_colour_ok ? kModeColored : kModeRanked);
+  // fp32 corner-unique hexes: two accumulator rows (4 barriers/batch) measured
+  // 1% faster than one row; fp64 keeps one row (shared memory)
+  const int corner_mode = sizeof(S) == 4 ? kModeCornerPhase2 : kModeCornerPhase;
+  int mode = P.corner_unique ? corner_mode : (hex_colour_ok ? kModeColored : kModeRanked);
   if (const char *env = getenv("FH_TILE_MODE")) {
     const int m = atoi(env);
     if (m == kModeRanked || m == kModeSharedAtomic || (m == kModeColored && hex_colour_ok) ||
-        ((m == kModeCornerPhase || m == kModeCornerSlot) && P.corner_unique))
+        ((m == kModeCornerPhase || m == kModeCornerSlot || m == kModeCornerPhase2) && P.corner_unique))
       mode = m;
   }
   // `mode` is the hex mode (kernel template); tets never are corner-unique and
@@ -572,7 +575,8 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   if (const char *env = getenv("FH_TILE_STAGES")) g.n_stages = std::min(kMaxStages, std::max(1, atoi(env)));
   g.smem_T = (int)al(2 * sizeof(S) * (size_t)std::max(1, P.max_local_nodes));
   // +1: the trash slot of the corner-phase accumulation
-  g.smem_acc = (int)al(sizeof(S) * (st->mode == kModeCornerSlot ? 8 : 1) * ((size_t)std::max(1, P.max_part_free) + 1));
+  const int rows = st->mode == kModeCornerSlot ? 8 : (st->mode == kModeCornerPhase2 ? 2 : 1);
+  g.smem_acc = (int)al(sizeof(S) * rows * ((size_t)std::max(1, P.max_part_free) + 1));
   int stage = 0;
   if (e->n_tet)
     stage = std::max(stage, StageBytes<S>(4, st->tet_kf.p || !e->td, tet_mode == kModeRanked, tet_mode == kModeColored));

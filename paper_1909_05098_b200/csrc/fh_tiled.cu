@@ -32,6 +32,13 @@ constexpr unsigned long long kNone = ~0ull;
 #define FH_MIN_BLOCKS_F32 4
 #endif
 constexpr int kMinBlocksF32 = FH_MIN_BLOCKS_F32;
+// global loads kept in flight per thread in the staging and node-update loops
+#ifndef FH_STAGE_UNROLL
+#define FH_STAGE_UNROLL 4
+#endif
+#ifndef FH_NODE_UNROLL
+#define FH_NODE_UNROLL 4
+#endif
 // corner phases: predicated accumulation (0) or unpredicated into a trash slot (1)
 #ifndef FH_TRASH_SLOT
 #define FH_TRASH_SLOT 0
@@ -262,7 +269,9 @@ __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned 
 //                batch needs as many barriers as it holds colours (1-2)
 //   kSharedAtomic  red.shared.add per corner, one barrier per batch: fastest
 //                but the summation order is not fixed (tolerance-only, opt-in)
-enum { kRanked = 0, kCornerPhase = 1, kCornerSlot = 2, kColored = 3, kSharedAtomic = 4 };
+//   kCornerPhase2  corner phases with two accumulator rows (corners a and
+//                a + N/2 share a phase): half the barriers, 2x accumulator smem
+enum { kRanked = 0, kCornerPhase = 1, kCornerSlot = 2, kColored = 3, kSharedAtomic = 4, kCornerPhase2 = 5 };
 
 template <typename S, int N, int MODE>
 __device__ __forceinline__ void accumulate(S *acc, const uint16_t (&nd)[kSPT][N], const S (&c)[kSPT][N], int nfree,
@@ -287,6 +296,19 @@ __device__ __forceinline__ void accumulate(S *acc, const uint16_t (&nd)[kSPT][N]
       for (int a = 0; a < N; ++a)
         if (loc[q][a] >= 0) atomicAdd(&acc[loc[q][a]], -c[q][a]);
     __syncthreads();  // stage buffer fully consumed before it is refilled
+  } else if (MODE == kCornerPhase2) {
+    // two accumulator rows: corner a (< N/2) into row 0, corner a + N/2 into
+    // row 1 in the same phase -> N/2 barriers per batch; F = row0 + row1
+    S *acc1 = acc + nfree;
+#pragma unroll
+    for (int a = 0; a < N / 2; ++a) {
+#pragma unroll
+      for (int q = 0; q < kSPT; ++q) {
+        if (loc[q][a] >= 0) acc[loc[q][a]] -= c[q][a];
+        if (loc[q][a + N / 2] >= 0) acc1[loc[q][a + N / 2]] -= c[q][a + N / 2];
+      }
+      __syncthreads();
+    }
   } else if (MODE == kCornerPhase && !FH_TRASH_SLOT) {
 #pragma unroll
     for (int a = 0; a < N; ++a) {
@@ -336,7 +358,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
   const int n0 = g.part_node_start[p];
   const int nn = g.part_node_start[p + 1] - n0;
   const int nfree = g.part_n_free[p];
-  const int nbt = (g.part_tet_count[p] + kBatch - 1) / kBatch;
+  // tile tables read once (the batch loop would otherwise re-load them every iteration)
+  const int t_cnt = __ldg(g.part_tet_count + p), h_cnt = __ldg(g.part_hex_count + p);
+  const int t_start = __ldg(g.part_tet_start + p), h_start = __ldg(g.part_hex_start + p);
+  const int nbt = (t_cnt + kBatch - 1) / kBatch;
   const int nbh = (g.part_hex_count[p] + kBatch - 1) / kBatch;
   const int nb = nbt + nbh;
   if (tid == 0) {
@@ -349,7 +374,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
   // stage temperatures: owned range + halo list; zero accumulators
   const bool kstage = TD && g.mats.n == 1;
   const Curve<S> &k0 = g.mats.m[0].k;
-  constexpr int U = 4;  // loads in flight per thread while staging
+  constexpr int U = FH_STAGE_UNROLL;  // loads in flight per thread while staging
   for (int base = tid; base < nn; base += U * kTileThreads) {
     S x[U];
 #pragma unroll
@@ -380,7 +405,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
       if (i < nh) sT[nn + i] = TK<S>{x[u], kstage ? interp(k0, x[u]) : S(0)};
     }
   }
-  for (int i = tid; i < (MODE == kCornerSlot ? 8 : 1) * nfree; i += kTileThreads) acc[i] = S(0);
+  for (int i = tid; i < (MODE == kCornerSlot ? 8 : (MODE == kCornerPhase2 ? 2 : 1)) * nfree; i += kTileThreads)
+    acc[i] = S(0);
   __syncthreads();
 
   int st = 0;
@@ -390,7 +416,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
     mbar_wait(&bars[st], parity);
     const bool tet = KINDS == 1 || (KINDS == 2 && j < nbt);
     const int b = tet ? j : j - nbt;
-    const int cnt = tet ? g.part_tet_count[p] : g.part_hex_count[p];
+    const int cnt = tet ? t_cnt : h_cnt;
     bool valid[kSPT];
 #pragma unroll
     for (int q = 0; q < kSPT; ++q) valid[q] = b * kBatch + q * kTileThreads + tid < cnt;
@@ -401,7 +427,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
 #pragma unroll
       for (int q = 0; q < kSPT; ++q) {
         const int i = q * kTileThreads + tid;
-        const int s = g.part_tet_start[p] + b * kBatch + i;
+        const int s = t_start + b * kBatch + i;
         const Curve<S> &kc = g.mats.m[(g.tet_region && valid[q]) ? g.tet_region[s] : 0].k;
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
@@ -424,7 +450,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
         }
       }
       accumulate<S, 4, kRanked>(acc, nd, c, nfree, valid, rk,
-                                g.tet_phase ? (int)g.tet_bnph[(g.part_tet_start[p] + b * kBatch) / kBatch]
+                                g.tet_phase ? (int)g.tet_bnph[(t_start + b * kBatch) / kBatch]
                                             : g.max_phase_tet);
     } else {
       uint16_t nd[kSPT][8];
@@ -433,7 +459,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
 #pragma unroll
       for (int q = 0; q < kSPT; ++q) {
         const int i = q * kTileThreads + tid;
-        const int s = g.part_hex_start[p] + b * kBatch + i;
+        const int s = h_start + b * kBatch + i;
         const Curve<S> &kc = g.mats.m[(g.hex_region && valid[q]) ? g.hex_region[s] : 0].k;
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
@@ -460,7 +486,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
       }
       if (MODE == kColored)
         accumulate<S, 8, kRanked>(acc, nd, c, nfree, valid, rk,
-                                  g.hex_bnph[(g.part_hex_start[p] + b * kBatch) / kBatch]);
+                                  g.hex_bnph[(h_start + b * kBatch) / kBatch]);
       else
         accumulate<S, 8, MODE>(acc, nd, c, nfree, valid, rk, g.max_phase_hex);
     }
@@ -479,7 +505,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
   // lumped nodal update of the owned free nodes
   bool bad = false;
   const int rstart = g.part_robin_start[p];
-  constexpr int UN = 4;  // nodes per thread per round: their global loads are issued together
+  constexpr int UN = FH_NODE_UNROLL;  // nodes per thread per round: their global loads are issued together
   for (int base = tid; base < nfree; base += UN * kTileThreads) {
     S v[UN], q[UN], cf[UN], kf[UN], px[UN], py[UN], pz[UN];
 #pragma unroll
@@ -506,6 +532,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
       if (MODE == kCornerSlot) {  // corner slots summed in fixed corner order: deterministic
         Fsum = ((acc[loc] + acc[nfree + loc]) + (acc[2 * nfree + loc] + acc[3 * nfree + loc])) +
                ((acc[4 * nfree + loc] + acc[5 * nfree + loc]) + (acc[6 * nfree + loc] + acc[7 * nfree + loc]));
+      } else if (MODE == kCornerPhase2) {
+        Fsum = acc[loc] + acc[nfree + loc];
       } else {
         Fsum = acc[loc];
       }
@@ -542,18 +570,18 @@ void tiled_step(const TiledArgs<S> &g, int n_parts, bool td, int mode_sel, size_
 #define FH_MODES(TDV, KV)                                                                          \
   {k_tiled_step<S, TDV, kRanked, KV>, k_tiled_step<S, TDV, kCornerPhase, KV>,                       \
    k_tiled_step<S, TDV, kCornerSlot, KV>, k_tiled_step<S, TDV, kColored, KV>,                       \
-   k_tiled_step<S, TDV, kSharedAtomic, KV>}
+   k_tiled_step<S, TDV, kSharedAtomic, KV>, k_tiled_step<S, TDV, kCornerPhase2, KV>}
 #define FH_TETONLY(TDV)                                                                            \
   {k_tiled_step<S, TDV, kRanked, 1>, k_tiled_step<S, TDV, kRanked, 1>, k_tiled_step<S, TDV, kRanked, 1>, \
-   k_tiled_step<S, TDV, kRanked, 1>, k_tiled_step<S, TDV, kRanked, 1>}
-  static const K table[2][3][5] = {{FH_MODES(false, 0), FH_TETONLY(false), FH_MODES(false, 2)},
+   k_tiled_step<S, TDV, kRanked, 1>, k_tiled_step<S, TDV, kRanked, 1>, k_tiled_step<S, TDV, kRanked, 1>}
+  static const K table[2][3][6] = {{FH_MODES(false, 0), FH_TETONLY(false), FH_MODES(false, 2)},
                                    {FH_MODES(true, 0), FH_TETONLY(true), FH_MODES(true, 2)}};
 #undef FH_MODES
 #undef FH_TETONLY
-  const int mode = mode_sel < 0 || mode_sel > 4 ? 0 : mode_sel;
+  const int mode = mode_sel < 0 || mode_sel > 5 ? 0 : mode_sel;
   const int kinds = (g.part_tet_start && g.tet_conn16 && g.hex_conn16) ? 2 : (g.hex_conn16 ? 0 : 1);
   const K kern = table[td ? 1 : 0][kinds][mode];
-  static size_t configured[2][3][5] = {};
+  static size_t configured[2][3][6] = {};
   size_t &cfg = configured[td ? 1 : 0][kinds][mode];
   if (smem > cfg) {
     FH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

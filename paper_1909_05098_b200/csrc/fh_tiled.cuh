@@ -72,7 +72,14 @@ void tiled_step(const TiledArgs<S> &g, int n_parts, bool td, int mode, size_t sm
 
 // accumulation mode of the step kernel (see fh_tiled.cu): 0 ranked phases,
 // 1 corner phases, 2 corner slots (the last two need corner-unique tiles)
-enum TileMode { kModeRanked = 0, kModeCornerPhase = 1, kModeCornerSlot = 2, kModeColored = 3, kModeSharedAtomic = 4 };
+enum TileMode {
+  kModeRanked = 0,
+  kModeCornerPhase = 1,
+  kModeCornerSlot = 2,
+  kModeColored = 3,
+  kModeSharedAtomic = 4,
+  kModeCornerPhase2 = 5
+};
 
 // TI freeze: per-slot kbar (global-id connectivity conn4/conn8) and per-node
 // capacity / perfusion from Tin.

@@ -4,7 +4,10 @@
 
 namespace fh {
 
-constexpr int kTileThreads = 256;  // threads per tile CTA
+#ifndef FH_TILE_THREADS
+#define FH_TILE_THREADS 256
+#endif
+constexpr int kTileThreads = FH_TILE_THREADS;  // threads per tile CTA
 constexpr int kSPT = 1;            // element slots per thread per batch (2 measured slower: smem)
 constexpr int kBatch = kTileThreads * kSPT;  // == partition batch size B
 constexpr int kMaxStages = 4;      // TMA ring depth limit (batches in flight per CTA)

@@ -244,10 +244,19 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    L2_BYTES = 126 * 2**20
+    flush_l2 = eng.layout()["step_bytes"] < 2 * L2_BYTES
     wall0 = time.time()
     elapsed = C.c_float(0.0)
-    # CUDA events recorded on the engine's launch stream around the K launches
-    rc = L.fh_step_timed(h, args.steps, dt, C.byref(rep), C.byref(elapsed))
+    if not flush_l2:
+        # CUDA events recorded on the engine's launch stream around the K launches
+        rc = L.fh_step_timed(h, args.steps, dt, C.byref(rep), C.byref(elapsed))
+    else:
+        # the step's working set fits in L2: a 2x-L2 buffer is overwritten on
+        # the engine stream before every step and each step is timed alone
+        scratch = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=f"cuda:{local}")
+        rc = L.fh_step_timed_flush(h, args.steps, dt, C.c_void_p(scratch.data_ptr()), scratch.numel(),
+                                   C.byref(rep), C.byref(elapsed))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -309,7 +318,8 @@ def main():
                    "assembly": "tiled", "parts": lay["n_parts"], "slots": lay["n_slots"],
                    "parallelism": f"{world} GPU domain decomposition (8 z-slab domains, NCCL halo exchange)"
                    if world > 1 else "1 GPU",
-                   "l2": "per-step input > 126 MB L2 (no flush needed)", "dt_s": dt, "setup_s": t_setup},
+                   "l2": ("working set < 2x L2: 252 MB buffer overwritten before every timed step" if flush_l2
+                          else "per-step input > 2x 126 MB L2 (no flush needed)"), "dt_s": dt, "setup_s": t_setup},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_kind": peak_kind,
                      "canonical_bytes_per_step": lay["canonical_bytes"], "layout_bytes_per_step": lay["step_bytes"]},

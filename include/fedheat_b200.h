@@ -180,6 +180,13 @@ int fh_step(fh_engine *e, int64_t nsteps, double dt, fh_report *rep);
  * launches; *elapsed_ms = device time of the nsteps steps. */
 int fh_step_timed(fh_engine *e, int64_t nsteps, double dt, fh_report *rep, float *elapsed_ms);
 
+/* benchmark variant for working sets that fit in L2: before each of the
+ * nsteps steps, `scratch` (device memory, scratch_bytes > L2) is overwritten
+ * on the engine's stream; *elapsed_ms = the sum of the per-step device times
+ * (the overwrites excluded). */
+int fh_step_timed_flush(fh_engine *e, int64_t nsteps, double dt, void *scratch, size_t scratch_bytes,
+                        fh_report *rep, float *elapsed_ms);
+
 /* same, with host I/O around it: upload T_in (n doubles), step, download
  * the new field into T_out -- the reference's ExplicitEngine.step contract
  * with host-resident state (used for the e2e measurement). */

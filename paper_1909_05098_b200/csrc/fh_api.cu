@@ -718,30 +718,58 @@ void exact_run(fh_engine *e, int64_t nsteps, double dt) {
   }
 }
 
-int do_step(fh_engine *e, int64_t nsteps, double dt, fh_report *rep, float *elapsed_ms = nullptr) {
-  if (nsteps < 0) fail(FH_ERR_CONFIG, "nsteps must be >= 0");
-  if (!(dt > 0.0) || !std::isfinite(dt)) fail(FH_ERR_CONFIG, "dt must be positive and finite");
-  const int64_t step0 = e->step_index;
-  const int cur0 = e->assembly == FH_ASSEMBLY_EXACT ? 0 : (e->precision == 32 ? e->tf->cur : e->tdd->cur);
-  cudaEvent_t ev[2] = {nullptr, nullptr};
-  if (elapsed_ms) {
-    FH_CUDA(cudaEventCreate(&ev[0]));
-    FH_CUDA(cudaEventCreate(&ev[1]));
-    FH_CUDA(cudaEventRecord(ev[0], e->stream));
-  }
+void run_steps(fh_engine *e, int64_t nsteps, double dt) {
   if (e->assembly == FH_ASSEMBLY_EXACT)
     exact_run(e, nsteps, dt);
   else if (e->precision == 32)
     tiled_run<float>(e, nsteps, dt);
   else
     tiled_run<double>(e, nsteps, dt);
+}
+
+int do_step(fh_engine *e, int64_t nsteps, double dt, fh_report *rep, float *elapsed_ms = nullptr,
+            void *scratch = nullptr, size_t scratch_bytes = 0) {
+  if (nsteps < 0) fail(FH_ERR_CONFIG, "nsteps must be >= 0");
+  if (!(dt > 0.0) || !std::isfinite(dt)) fail(FH_ERR_CONFIG, "dt must be positive and finite");
+  const int64_t step0 = e->step_index;
+  const int cur0 = e->assembly == FH_ASSEMBLY_EXACT ? 0 : (e->precision == 32 ? e->tf->cur : e->tdd->cur);
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> sev;  // per-step start/stop events (L2-flushed timing)
+  if (elapsed_ms && !scratch) {
+    FH_CUDA(cudaEventCreate(&ev[0]));
+    FH_CUDA(cudaEventCreate(&ev[1]));
+    FH_CUDA(cudaEventRecord(ev[0], e->stream));
+  }
+  if (scratch) {
+    sev.resize(2 * nsteps);
+    for (auto &v : sev) FH_CUDA(cudaEventCreate(&v));
+    for (int64_t k = 0; k < nsteps; ++k) {
+      FH_CUDA(cudaMemsetAsync(scratch, (int)(k & 0xff), scratch_bytes, e->stream));
+      FH_CUDA(cudaEventRecord(sev[2 * k], e->stream));
+      run_steps(e, 1, dt);
+      FH_CUDA(cudaEventRecord(sev[2 * k + 1], e->stream));
+    }
+  } else {
+    run_steps(e, nsteps, dt);
+  }
+  if (scratch) {
+    if (!sev.empty()) FH_CUDA(cudaEventSynchronize(sev.back()));
+    float tot = 0.f;
+    for (int64_t k = 0; k < nsteps; ++k) {
+      float ms = 0.f;
+      FH_CUDA(cudaEventElapsedTime(&ms, sev[2 * k], sev[2 * k + 1]));
+      tot += ms;
+    }
+    for (auto &v : sev) cudaEventDestroy(v);
+    if (elapsed_ms) *elapsed_ms = tot;
+  }
   if (e->halo_pending) {  // the last step is complete once its halo has landed
     FH_CUDA(cudaStreamWaitEvent(e->stream, e->ev_halo, 0));
     e->halo_pending = false;
   }
   if (e->comm)  // every rank agrees on the first failing step
     nccl_min_u64(e->comm, &e->flag.p->step, e->stream);
-  if (elapsed_ms) {
+  if (elapsed_ms && !scratch) {
     FH_CUDA(cudaEventRecord(ev[1], e->stream));
     FH_CUDA(cudaEventSynchronize(ev[1]));
     FH_CUDA(cudaEventElapsedTime(elapsed_ms, ev[0], ev[1]));
@@ -1051,6 +1079,15 @@ int fh_step_timed(fh_engine *e, int64_t nsteps, double dt, fh_report *rep, float
   FH_API_BEGIN
   check_engine(e);
   return do_step(e, nsteps, dt, rep, elapsed_ms);
+  FH_API_END
+}
+
+int fh_step_timed_flush(fh_engine *e, int64_t nsteps, double dt, void *scratch, size_t scratch_bytes,
+                        fh_report *rep, float *elapsed_ms) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (!scratch || !scratch_bytes) fail(FH_ERR_CONFIG, "scratch buffer required");
+  return do_step(e, nsteps, dt, rep, elapsed_ms, scratch, scratch_bytes);
   FH_API_END
 }
 

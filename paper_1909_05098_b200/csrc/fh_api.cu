@@ -242,6 +242,28 @@ TiledState<float> &tstate<float>(fh_engine *e) { return *e->tf; }
 template <>
 TiledState<double> &tstate<double>(fh_engine *e) { return *e->tdd; }
 
+// Tiled kernels: a one-knot curve becomes the two-knot curve (y0, y0) with
+// slope 0 (same values everywhere).  Returns 1 when every curve of every
+// material then has exactly two knots (branch-free interpolation kernels).
+template <typename S>
+int normalise_curves(MatSet<S> &ms) {
+  int lin = 1;
+  for (int r = 0; r < ms.n; ++r) {
+    Curve<S> *cs[4] = {&ms.m[r].rho, &ms.m[r].c, &ms.m[r].k, &ms.m[r].wb};
+    for (Curve<S> *c : cs) {
+      if (c->n == 0) continue;  // no perfusion law (constant perfusion)
+      if (c->n == 1) {
+        c->n = 2;
+        c->x[1] = c->x[0];
+        c->y[1] = c->y[0];
+        c->slope[0] = S(0);
+      }
+      if (c->n != 2) lin = 0;
+    }
+  }
+  return lin;
+}
+
 template <typename S>
 MatSet<S> &mats_of(fh_engine *e);
 template <>
@@ -564,7 +586,9 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.robin_hA = st->robin_hA.p;
   g.robin_hAT = st->robin_hAT.p;
   g.mats = mats_of<S>(e);
-  g.n_src = (int)e->sources.size();
+  g.lin = normalise_curves(g.mats);
+  g.n_src = 0;  // set per step from the active sources
+  g.n_gauss = 0;
   g.runaway_limit = (S)e->runaway_limit;
   g.flag = e->flag.p;
   auto al = [](size_t b) { return (b + 127) & ~(size_t)127; };
@@ -647,19 +671,26 @@ void tiled_run(fh_engine *e, int64_t nsteps, double dt) {
     }
     g.dt = (S)dt;
     g.step_no = (unsigned long long)(e->step_index + 1);
-    for (int q = 0; q < g.n_src; ++q) {
-      const fh_source &src = e->sources[q];
-      SourceT<S> &d = g.src[q];
-      d.kind = src.kind;
-      d.active = (src.t0 <= t && t < src.t1);
-      d.amp = (S)src.amp;
-      d.inv2s2 = (S)(1.0 / (2.0 * src.sigma * src.sigma));
-      d.cap = (S)src.cap;
-      d.inv4pi_amp = (S)(src.amp / (4.0 * M_PI));
-      d.cx = (S)(src.x0[0] + src.vel[0] * t);
-      d.cy = (S)(src.x0[1] + src.vel[1] * t);
-      d.cz = (S)(src.x0[2] + src.vel[2] * t);
+    // active sources only, Gaussians first (the kernel loops over each kind
+    // without per-source branches)
+    int ns = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (const fh_source &src : e->sources) {
+        if ((src.kind == FH_SOURCE_GAUSSIAN) != (pass == 0) || !(src.t0 <= t && t < src.t1)) continue;
+        SourceT<S> &d = g.src[ns++];
+        d.kind = src.kind;
+        d.active = 1;
+        d.amp = (S)src.amp;
+        d.inv2s2 = (S)(1.0 / (2.0 * src.sigma * src.sigma));
+        d.cap = (S)src.cap;
+        d.inv4pi_amp = (S)(src.amp / (4.0 * M_PI));
+        d.cx = (S)(src.x0[0] + src.vel[0] * t);
+        d.cy = (S)(src.x0[1] + src.vel[1] * t);
+        d.cz = (S)(src.x0[2] + src.vel[2] * t);
+      }
+      if (pass == 0) g.n_gauss = ns;
     }
+    g.n_src = ns;
     if (e->X.world == 1) {
       g.part_begin = 0;
       tiled_step(g, st.n_parts_local, e->td, st.mode, st.smem, e->stream);
@@ -1164,7 +1195,6 @@ int fh_set_sources(fh_engine *e, const fh_source *sources, int32_t n) {
         FH_CUDA(cudaGetLastError());
         st.args.xyzv = st.xyz.p;
       }
-      st.args.n_src = n;
     };
     if (e->precision == 32) setup(*e->tf); else setup(*e->tdd);
     FH_CUDA(cudaStreamSynchronize(e->stream));

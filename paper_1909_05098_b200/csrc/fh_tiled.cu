@@ -98,12 +98,22 @@ struct StageLayout {
   }
 };
 
-template <typename S>
+// LIN: every curve has two knots (one-knot curves were normalised on the host
+// to y1 = y0, slope 0), so the clamped interpolation is two selects and an FMA
+template <bool LIN, typename S>
+__device__ __forceinline__ S ip(const Curve<S> &c, S x) {
+  if (!LIN) return interp(c, x);
+  S r = c.slope[0] * (x - c.x[0]) + c.y[0];
+  r = (x >= c.x[1]) ? c.y[1] : r;
+  return (x <= c.x[0]) ? c.y[0] : r;
+}
+
+template <bool LIN, typename S>
 __device__ __forceinline__ S kbar_from(const Curve<S> &kc, const S *Tn, int n, S kf) {
   S s = S(0);
 #pragma unroll
   for (int b = 0; b < 8; ++b)
-    if (b < n) s += interp(kc, Tn[b]);
+    if (b < n) s += ip<LIN>(kc, Tn[b]);
   return s / S(n) * kf;
 }
 
@@ -123,12 +133,12 @@ __device__ __forceinline__ double fast_exp(double x) { return exp(x); }
 
 // F - kb T + qb + qm + q_ext with C, kb from the material laws (TD) or the
 // frozen arrays (TI); returns the rate, writes the capacity
-template <typename S, bool TD>
+template <typename S, bool TD, bool LIN>
 __device__ __forceinline__ S node_rate(const Mat<S> &m, S x, S F, S v, S q, S cfrozen, S kbfrozen, S &cap) {
   S kb;
   if (TD) {
-    cap = interp(m.rho, x) * interp(m.c, x) * v;
-    kb = m.td_perf ? interp(m.wb, x) * m.cb * v : m.wbcb * v;
+    cap = ip<LIN>(m.rho, x) * ip<LIN>(m.c, x) * v;
+    kb = m.td_perf ? ip<LIN>(m.wb, x) * m.cb * v : m.wbcb * v;
   } else {
     cap = cfrozen;
     kb = m.td_perf ? kbfrozen : m.wbcb * v;
@@ -138,17 +148,20 @@ __device__ __forceinline__ S node_rate(const Mat<S> &m, S x, S F, S v, S q, S cf
 
 template <typename S>
 __device__ __forceinline__ S sources_at(const TiledArgs<S> &g, const S *xyz) {
+  // the host passes the active sources only, Gaussians first
   const S x = xyz[0], y = xyz[1], z = xyz[2];
   S q = S(0);
-  for (int k = 0; k < g.n_src; ++k) {
+  for (int k = 0; k < g.n_gauss; ++k) {
     const SourceT<S> &s = g.src[k];
-    if (!s.active) continue;
     const S dx = x - s.cx, dy = y - s.cy, dz = z - s.cz;
     const S r2 = (dx * dx + dy * dy) + dz * dz;
-    if (s.kind == FH_SOURCE_GAUSSIAN)
-      q += s.amp * fast_exp(-r2 * s.inv2s2);
-    else
-      q += r2 > S(0) ? min(s.cap, s.inv4pi_amp / r2) : s.cap;
+    q += s.amp * fast_exp(-r2 * s.inv2s2);
+  }
+  for (int k = g.n_gauss; k < g.n_src; ++k) {
+    const SourceT<S> &s = g.src[k];
+    const S dx = x - s.cx, dy = y - s.cy, dz = z - s.cz;
+    const S r2 = (dx * dx + dy * dy) + dz * dz;
+    q += r2 > S(0) ? min(s.cap, s.inv4pi_amp / r2) : s.cap;
   }
   return q;
 }
@@ -186,7 +199,7 @@ __device__ void issue_batch(const TiledArgs<S> &g, int p, int j, int nbt, unsign
 }
 
 // element loads of staged slot i of the batch ------------------------------------
-template <typename S, bool TD>
+template <typename S, bool TD, bool LIN>
 __device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned char *stage, const TK<S> *sT,
                                           const Curve<S> &kc, bool has_kf, int i, uint16_t nd[8], S c[8]) {
   const StageLayout<S> L(8, has_kf, g.hex_rank != nullptr);
@@ -210,7 +223,7 @@ __device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned 
       const S sum = ((K[0] + K[1]) + (K[2] + K[3])) + ((K[4] + K[5]) + (K[6] + K[7]));
       kb = sum * S(0.125) * kf;
     } else {
-      kb = kbar_from(kc, T, 8, kf);
+      kb = kbar_from<LIN>(kc, T, 8, kf);
     }
   }
   // g = sum_b s_b (T_b - T_0) with the corner signs of element.py HEX_VERTEX_SIGNS
@@ -226,7 +239,7 @@ __device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned 
   c[4] = -a + w2; c[5] = b2 + w2; c[6] = a + w2; c[7] = -b2 + w2;
 }
 
-template <typename S, bool TD>
+template <typename S, bool TD, bool LIN>
 __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned char *stage, const TK<S> *sT,
                                           const Curve<S> &kc, bool has_kf, int i, uint16_t nd[4], S c[4]) {
   const StageLayout<S> L(4, has_kf, g.tet_rank != nullptr);
@@ -248,7 +261,7 @@ __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned 
     if (g.mats.n == 1) {
       kb = ((K[0] + K[1]) + (K[2] + K[3])) * S(0.25) * kf;
     } else {
-      kb = kbar_from(kc, T, 4, kf);
+      kb = kbar_from<LIN>(kc, T, 4, kf);
     }
   }
   const S d1 = T[1] - T[0], d2 = T[2] - T[0], d3 = T[3] - T[0];
@@ -343,7 +356,7 @@ __device__ __forceinline__ void accumulate(S *acc, const uint16_t (&nd)[kSPT][N]
   }
 }
 // KINDS: 0 hex-only, 1 tet-only, 2 mixed mesh (the absent kind's path is compiled out)
-template <typename S, bool TD, int MODE, int KINDS>
+template <typename S, bool TD, int MODE, int KINDS, bool LIN>
 __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 : 2) k_tiled_step(const __grid_constant__ TiledArgs<S> g) {
   extern __shared__ __align__(128) unsigned char smem[];
   TK<S> *sT = reinterpret_cast<TK<S> *>(smem);
@@ -385,7 +398,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = base + u * kTileThreads;
-      if (i < nn) sT[i] = TK<S>{x[u], kstage ? interp(k0, x[u]) : S(0)};
+      if (i < nn) sT[i] = TK<S>{x[u], kstage ? ip<LIN>(k0, x[u]) : S(0)};
     }
   }
   const int h0 = g.part_halo_start[p], nh = g.part_halo_start[p + 1] - h0;
@@ -402,7 +415,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = base + u * kTileThreads;
-      if (i < nh) sT[nn + i] = TK<S>{x[u], kstage ? interp(k0, x[u]) : S(0)};
+      if (i < nh) sT[nn + i] = TK<S>{x[u], kstage ? ip<LIN>(k0, x[u]) : S(0)};
     }
   }
   for (int i = tid; i < (MODE == kCornerSlot ? 8 : (MODE == kCornerPhase2 ? 2 : 1)) * nfree; i += kTileThreads)
@@ -435,7 +448,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
           c[q][a] = S(0);
           rk[q][a] = 0xff;
         }
-        if (valid[q]) tet_loads<S, TD>(g, stage, sT, kc, g.tet_kf != nullptr, i, nd[q], c[q]);
+        if (valid[q]) tet_loads<S, TD, LIN>(g, stage, sT, kc, g.tet_kf != nullptr, i, nd[q], c[q]);
         // tets are never corner-unique: colour phases (phase byte per slot) or,
         // if the colouring overflowed, ranked phases (rank byte per corner)
         if (valid[q] && g.tet_phase) {
@@ -467,7 +480,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
           c[q][a] = S(0);
           rk[q][a] = 0xff;
         }
-        if (valid[q]) hex_loads<S, TD>(g, stage, sT, kc, g.hex_kf != nullptr, i, nd[q], c[q]);
+        if (valid[q]) hex_loads<S, TD, LIN>(g, stage, sT, kc, g.hex_kf != nullptr, i, nd[q], c[q]);
         if (MODE == kRanked && valid[q]) {
           const StageLayout<S> L(8, g.hex_kf != nullptr, true);
           const uint2 w = reinterpret_cast<const uint2 *>(stage + L.rank)[i];
@@ -541,9 +554,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
       S cap;
       // single material: curve parameters are uniform kernel-parameter operands
       if (!g.node_region)
-        rate = node_rate<S, TD>(g.mats.m[0], x, Fsum, v[u], q[u], cf[u], kf[u], cap);
+        rate = node_rate<S, TD, LIN>(g.mats.m[0], x, Fsum, v[u], q[u], cf[u], kf[u], cap);
       else
-        rate = node_rate<S, TD>(g.mats.m[g.node_region[n]], x, Fsum, v[u], q[u], cf[u], kf[u], cap);
+        rate = node_rate<S, TD, LIN>(g.mats.m[g.node_region[n]], x, Fsum, v[u], q[u], cf[u], kf[u], cap);
       if (g.n_src) {
         const S xyz[3] = {px[u], py[u], pz[u]};
         rate += sources_at(g, xyz) * v[u];
@@ -566,23 +579,29 @@ template <typename S>
 void tiled_step(const TiledArgs<S> &g, int n_parts, bool td, int mode_sel, size_t smem, cudaStream_t s) {
   if (n_parts <= 0) return;
   using K = void (*)(TiledArgs<S>);
-  // [td][kinds][hex mode]; tet-only meshes ignore the hex mode
-#define FH_MODES(TDV, KV)                                                                          \
-  {k_tiled_step<S, TDV, kRanked, KV>, k_tiled_step<S, TDV, kCornerPhase, KV>,                       \
-   k_tiled_step<S, TDV, kCornerSlot, KV>, k_tiled_step<S, TDV, kColored, KV>,                       \
-   k_tiled_step<S, TDV, kSharedAtomic, KV>, k_tiled_step<S, TDV, kCornerPhase2, KV>}
-#define FH_TETONLY(TDV)                                                                            \
-  {k_tiled_step<S, TDV, kRanked, 1>, k_tiled_step<S, TDV, kRanked, 1>, k_tiled_step<S, TDV, kRanked, 1>, \
-   k_tiled_step<S, TDV, kRanked, 1>, k_tiled_step<S, TDV, kRanked, 1>, k_tiled_step<S, TDV, kRanked, 1>}
-  static const K table[2][3][6] = {{FH_MODES(false, 0), FH_TETONLY(false), FH_MODES(false, 2)},
-                                   {FH_MODES(true, 0), FH_TETONLY(true), FH_MODES(true, 2)}};
+  // [lin][td][kinds][hex mode]; tet-only meshes ignore the hex mode.  LIN
+  // only matters with temperature-dependent laws (TI never interpolates).
+#define FH_MODES(TDV, KV, L)                                                                       \
+  {k_tiled_step<S, TDV, kRanked, KV, L>, k_tiled_step<S, TDV, kCornerPhase, KV, L>,                 \
+   k_tiled_step<S, TDV, kCornerSlot, KV, L>, k_tiled_step<S, TDV, kColored, KV, L>,                 \
+   k_tiled_step<S, TDV, kSharedAtomic, KV, L>, k_tiled_step<S, TDV, kCornerPhase2, KV, L>}
+#define FH_TETONLY(TDV, L)                                                                         \
+  {k_tiled_step<S, TDV, kRanked, 1, L>, k_tiled_step<S, TDV, kRanked, 1, L>,                        \
+   k_tiled_step<S, TDV, kRanked, 1, L>, k_tiled_step<S, TDV, kRanked, 1, L>,                        \
+   k_tiled_step<S, TDV, kRanked, 1, L>, k_tiled_step<S, TDV, kRanked, 1, L>}
+  static const K table[2][2][3][6] = {
+      {{FH_MODES(false, 0, false), FH_TETONLY(false, false), FH_MODES(false, 2, false)},
+       {FH_MODES(true, 0, false), FH_TETONLY(true, false), FH_MODES(true, 2, false)}},
+      {{FH_MODES(false, 0, false), FH_TETONLY(false, false), FH_MODES(false, 2, false)},
+       {FH_MODES(true, 0, true), FH_TETONLY(true, true), FH_MODES(true, 2, true)}}};
 #undef FH_MODES
 #undef FH_TETONLY
   const int mode = mode_sel < 0 || mode_sel > 5 ? 0 : mode_sel;
   const int kinds = (g.part_tet_start && g.tet_conn16 && g.hex_conn16) ? 2 : (g.hex_conn16 ? 0 : 1);
-  const K kern = table[td ? 1 : 0][kinds][mode];
-  static size_t configured[2][3][6] = {};
-  size_t &cfg = configured[td ? 1 : 0][kinds][mode];
+  const int lin = g.lin ? 1 : 0;
+  const K kern = table[lin][td ? 1 : 0][kinds][mode];
+  static size_t configured[2][2][3][6] = {};
+  size_t &cfg = configured[lin][td ? 1 : 0][kinds][mode];
   if (smem > cfg) {
     FH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cfg = smem;
@@ -603,7 +622,7 @@ __global__ void k_freeze_slots(const TiledArgs<S> g, const int32_t *__restrict__
   S T[8];
 #pragma unroll
   for (int b = 0; b < 8; ++b) T[b] = b < N ? g.Tin[conn[N * s + b]] : S(0);
-  kbar[s] = kbar_from(kc, T, N, kf ? kf[s] : S(1));
+  kbar[s] = kbar_from<false>(kc, T, N, kf ? kf[s] : S(1));
 }
 
 template <typename S>

@@ -52,7 +52,9 @@ struct TiledArgs {
   const S *xyzv;                    // (x, y, z, v) per node, for time-dependent sources
   const uint8_t *node_region;
   const S *robin_hA, *robin_hAT;
-  MatSet<S> mats;
+  MatSet<S> mats;   // one-knot curves normalised to two knots (see normalise_curves)
+  int lin;          // every curve has <= 2 knots: branch-free interpolation kernels
+  int n_gauss;      // active sources, Gaussians first: src[0, n_gauss) Gaussian, [n_gauss, n_src) RF
   int n_src;
   SourceT<S> src[kMaxSources];
   S dt, runaway_limit;

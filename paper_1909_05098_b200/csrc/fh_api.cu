@@ -396,6 +396,9 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   if (o.part_nodes <= 0 && V / pin.target_part_nodes < 2 * 148)
     pin.target_part_nodes = (int)std::max<int64_t>(96, V / (2 * 148));
   pin.batch = kBatch;
+  // layout tuning knobs (scripts/sweep.py): hex colour order, first-touch node order
+  if (const char *env = getenv("FH_HEX_COLOR")) pin.hex_color = atoi(env);
+  if (const char *env = getenv("FH_FIRST_TOUCH")) pin.first_touch = atoi(env);
   pin.n_domains = std::max(1, o.n_domains);
   pin.slab_axis = o.slab_axis;
   build_partition(pin, e->part);
@@ -1605,6 +1608,9 @@ int fh_plan_create(const fh_mesh *mesh, const fh_boundary *bnd, const fh_options
   pin.node_class = cls.data();
   pin.target_part_nodes = opts->part_nodes > 0 ? opts->part_nodes : (opts->precision == 32 ? 1536 : 768);
   pin.batch = kBatch;
+  // layout tuning knobs (scripts/sweep.py): hex colour order, first-touch node order
+  if (const char *env = getenv("FH_HEX_COLOR")) pin.hex_color = atoi(env);
+  if (const char *env = getenv("FH_FIRST_TOUCH")) pin.first_touch = atoi(env);
   pin.n_domains = std::max(1, opts->n_domains);
   pin.slab_axis = opts->slab_axis;
   build_partition(pin, pl->P);

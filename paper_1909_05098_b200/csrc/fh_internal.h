@@ -126,6 +126,8 @@ struct PartitionInput {
   int batch;          // slots per batch (== kernel block size)
   int n_domains;      // top-level domain count (parts never straddle domains)
   int slab_axis;      // -1 RCB, else domains are slabs along this axis
+  int hex_color = 0;  // 0: colour hexes only when not corner-unique; 1: always
+  int first_touch = 0;  // renumber each tile's nodes in first-touch order of its batches (measured neutral)
 };
 
 struct Partition {

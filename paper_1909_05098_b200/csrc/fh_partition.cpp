@@ -268,7 +268,7 @@ void build_partition(const PartitionInput &in, Partition &P) {
         }
       }
     }
-    P.hex_colored = !hex_unique;
+    P.hex_colored = !hex_unique || in.hex_color == 1;
     P.tet_color.clear();
     P.hex_color.clear();
     tet_color_pp.assign(P.n_parts, {});
@@ -279,6 +279,54 @@ void build_partition(const PartitionInput &in, Partition &P) {
         for (auto &x : colour_part(hex_pp[p], 8, p)) hex_color_pp[p].push_back((uint8_t)x.first);
       else
         hex_color_pp[p].assign(hex_pp[p].size(), 0);
+    }
+  }
+  // 4b. node order inside each tile by first touch: scanning the tile's
+  //     batches corner by corner (corner a of every slot of the batch, then
+  //     corner a + 1), each node gets the next id of its class the first time
+  //     it is met.  Neighbouring threads then gather neighbouring shared-memory
+  //     words for every corner, whatever the slot order (colour or min
+  //     corner), so the gathers and accumulations stay bank-conflict free.
+  //     The class ranges (free | robin | dirichlet) are kept.
+  if (in.first_touch) {
+    const size_t Bt = (size_t)std::max(1, in.batch);
+    std::vector<int32_t> touch(P.max_part_nodes);
+    std::vector<int32_t> loc;
+    std::vector<int64_t> olds;
+    for (int p = 0; p < P.n_parts; ++p) {
+      const int64_t n0 = P.part_node_start[p], nn = P.part_node_start[p + 1] - n0;
+      std::fill(touch.begin(), touch.begin() + nn, -1);
+      int32_t k = 0;
+      auto scan = [&](const std::vector<int32_t> &v, int N) {
+        for (size_t b = 0; b < v.size(); b += Bt) {
+          const size_t be = std::min(v.size(), b + Bt);
+          for (int a = 0; a < N; ++a)
+            for (size_t q = b; q < be; ++q) {
+              const int32_t e = v[q];
+              const int64_t *c = N == 4 ? in.tets + 4 * (int64_t)e : in.hexes + 8 * ((int64_t)e - in.n_tet);
+              const int64_t l = P.new_of_old[c[a]] - n0;
+              if (l >= 0 && l < nn && touch[l] < 0) touch[l] = k++;
+            }
+        }
+      };
+      scan(tet_pp[p], 4);
+      scan(hex_pp[p], 8);
+      for (int64_t i = 0; i < nn; ++i)
+        if (touch[i] < 0) touch[i] = k++;
+      const int64_t rs = P.part_robin_start[p], nf = P.part_n_free[p];
+      auto cls_of = [rs, nf](int64_t i) { return i < rs ? 0 : (i < nf ? 1 : 2); };
+      loc.resize(nn);
+      std::iota(loc.begin(), loc.end(), 0);
+      std::sort(loc.begin(), loc.end(), [&](int32_t x, int32_t y) {
+        const int cx = cls_of(x), cy = cls_of(y);
+        return cx < cy || (cx == cy && touch[x] < touch[y]);
+      });
+      olds.resize(nn);
+      for (int64_t j = 0; j < nn; ++j) olds[j] = P.old_of_new[n0 + loc[j]];
+      for (int64_t j = 0; j < nn; ++j) {
+        P.old_of_new[n0 + j] = olds[j];
+        P.new_of_old[olds[j]] = n0 + j;
+      }
     }
   }
   P.part_tet_start.assign(P.n_parts + 1, 0);
@@ -325,7 +373,8 @@ void build_partition(const PartitionInput &in, Partition &P) {
   P.max_local_nodes = 0;
   P.max_part_free = 0;
   {
-    std::vector<int32_t> halo;
+    std::vector<int32_t> halo, hrank, hord;
+    const int32_t B0 = std::max(1, in.batch);
     for (int p = 0; p < P.n_parts; ++p) {
       const int32_t n0 = P.part_node_start[p], nn = P.part_node_start[p + 1] - n0;
       halo.clear();
@@ -339,19 +388,44 @@ void build_partition(const PartitionInput &in, Partition &P) {
       collect(P.hex_conn, 8, P.part_hex_start[p], P.part_hex_count[p]);
       std::sort(halo.begin(), halo.end());
       halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
+      // staging order of the halo (sT[nn + i] = T[hord[i]]): first touch, like the owned nodes
+      hrank.assign(halo.size(), -1);
+      {
+        int32_t k = 0;
+        auto scan = [&](const std::vector<int32_t> &conn, int N, int32_t s0, int32_t cnt) {
+          for (int32_t b = 0; b < cnt; b += B0) {
+            const int32_t be = std::min(cnt, b + B0);
+            for (int a = 0; a < N; ++a)
+              for (int32_t q = b; q < be; ++q) {
+                const int32_t n = conn[(size_t)N * (s0 + q) + a];
+                if (n >= n0 && n < n0 + nn) continue;
+                const size_t h = std::lower_bound(halo.begin(), halo.end(), n) - halo.begin();
+                if (hrank[h] < 0) hrank[h] = k++;
+              }
+          }
+        };
+        if (in.first_touch) {
+          scan(P.tet_conn, 4, P.part_tet_start[p], P.part_tet_count[p]);
+          scan(P.hex_conn, 8, P.part_hex_start[p], P.part_hex_count[p]);
+        } else {
+          for (size_t h = 0; h < halo.size(); ++h) hrank[h] = (int32_t)h;
+        }
+      }
+      hord.resize(halo.size());
+      for (size_t h = 0; h < halo.size(); ++h) hord[hrank[h]] = halo[h];
       const int64_t nloc = (int64_t)nn + (int64_t)halo.size();
       if (nloc >= 0xffff) fail(FH_ERR_CONFIG, "tile has too many local nodes; lower part_nodes");
       P.max_local_nodes = std::max<int>(P.max_local_nodes, (int)nloc);
       P.max_part_free = std::max<int>(P.max_part_free, P.part_n_free[p]);
       auto local = [&](int32_t n) -> uint16_t {
         if (n >= n0 && n < n0 + nn) return (uint16_t)(n - n0);
-        return (uint16_t)(nn + (std::lower_bound(halo.begin(), halo.end(), n) - halo.begin()));
+        return (uint16_t)(nn + hrank[std::lower_bound(halo.begin(), halo.end(), n) - halo.begin()]);
       };
       for (int64_t q = 4 * (int64_t)P.part_tet_start[p]; q < 4 * (int64_t)(P.part_tet_start[p] + P.part_tet_count[p]); ++q)
         P.tet_conn16[q] = local(P.tet_conn[q]);
       for (int64_t q = 8 * (int64_t)P.part_hex_start[p]; q < 8 * (int64_t)(P.part_hex_start[p] + P.part_hex_count[p]); ++q)
         P.hex_conn16[q] = local(P.hex_conn[q]);
-      P.halo_nodes.insert(P.halo_nodes.end(), halo.begin(), halo.end());
+      P.halo_nodes.insert(P.halo_nodes.end(), hord.begin(), hord.end());
       P.part_halo_start[p + 1] = (int32_t)P.halo_nodes.size();
     }
   }

@@ -57,17 +57,44 @@ def restated_partition(mesh, dirichlet, robin, n_domains, target, slab_axis=-1):
 @pytest.mark.parametrize("kind,div,ndom,target,slab", [("hex", 9, 1, 100, -1), ("tet", 6, 2, 64, -1),
                                                       ("hex", 10, 8, 150, -1), ("hex", 12, 4, 200, 2),
                                                       ("tet", 5, 8, 40, 2)])
-def test_partition_matches_restatement_bitwise(kind, div, ndom, target, slab):
+def test_partition_matches_restatement_bitwise(kind, div, ndom, target, slab, monkeypatch):
     mesh = fh.jittered_cube_mesh(kind, div, 0.1, 0.2, seed=div)
     bnd = fh.BoundarySpec(dirichlet=(("z0", 37.0), ("x1", 37.0)))
-    plan = Plan(mesh, MAT, bnd, world=1, rank=0, n_domains=ndom, part_nodes=target, slab_axis=slab)
-    dn = plan.boundary.dirichlet_nodes
+    # default (no first-touch pass): the order is exactly (part, class, original id)
+    plan0 = Plan(mesh, MAT, bnd, world=1, rank=0, n_domains=ndom, part_nodes=target, slab_axis=slab)
+    dn = plan0.boundary.dirichlet_nodes
     n2o, bounds = restated_partition(mesh, dn, np.empty(0, np.int64), ndom, target, slab)
-    assert np.array_equal(plan.new_to_old, n2o)
+    assert np.array_equal(plan0.new_to_old, n2o)
+    assert np.array_equal(plan0.part_node_start, bounds)
+    # first-touch order: same tiles and class ranges, nodes permuted inside each class
+    monkeypatch.setenv("FH_FIRST_TOUCH", "1")
+    plan = Plan(mesh, MAT, bnd, world=1, rank=0, n_domains=ndom, part_nodes=target, slab_axis=slab)
     assert np.array_equal(plan.part_node_start, bounds)
+    cls = np.zeros(mesh.n_nodes, np.int64)
+    cls[dn] = 2
+    for p in range(len(bounds) - 1):
+        a, b = plan.new_to_old[bounds[p]:bounds[p + 1]], n2o[bounds[p]:bounds[p + 1]]
+        assert np.array_equal(cls[a], cls[b])  # class ranges kept
+        assert np.array_equal(np.sort(a), np.sort(b))
     # same input -> same plan
     again = Plan(mesh, MAT, bnd, world=1, rank=0, n_domains=ndom, part_nodes=target, slab_axis=slab)
     assert np.array_equal(again.new_to_old, plan.new_to_old)
+
+
+def test_first_touch_order_makes_batch_gathers_contiguous(monkeypatch):
+    """Structured hex tile: corner a of consecutive slots of a batch maps to
+    consecutive node ids (csrc/fh_partition.cpp step 4b)."""
+    mesh = fh.generate_cube_mesh("hex", 12, 0.1)
+    monkeypatch.setenv("FH_FIRST_TOUCH", "1")
+    plan = Plan(mesh, MAT, n_domains=1, part_nodes=4096)
+    assert plan.info["n_parts"] == 1
+    o2n = np.empty(mesh.n_nodes, np.int64)
+    o2n[plan.new_to_old] = np.arange(mesh.n_nodes)
+    conn = o2n[mesh.hexes]
+    # first batch of slots = the first 256 elements in min-corner order
+    order = np.argsort(conn.min(axis=1), kind="stable")[:256]
+    steps = np.diff(conn[order], axis=0)
+    assert np.mean(steps == 1) > 0.9
 
 
 def test_structured_hex_is_corner_unique_and_tets_are_coloured():

@@ -34,10 +34,10 @@ constexpr unsigned long long kNone = ~0ull;
 constexpr int kMinBlocksF32 = FH_MIN_BLOCKS_F32;
 // global loads kept in flight per thread in the staging and node-update loops
 #ifndef FH_STAGE_UNROLL
-#define FH_STAGE_UNROLL 4
+#define FH_STAGE_UNROLL 8
 #endif
 #ifndef FH_NODE_UNROLL
-#define FH_NODE_UNROLL 4
+#define FH_NODE_UNROLL 2
 #endif
 // corner phases: predicated accumulation (0) or unpredicated into a trash slot (1)
 #ifndef FH_TRASH_SLOT
@@ -150,13 +150,20 @@ template <typename S>
 __device__ __forceinline__ S sources_at(const TiledArgs<S> &g, const S *xyz) {
   // the host passes the active sources only, Gaussians first
   const S x = xyz[0], y = xyz[1], z = xyz[2];
+  if (g.n_src == 1 && g.n_gauss == 1) {  // the common single-Gaussian case, straight-line
+    const SourceT<S> &s = g.src[0];
+    const S dx = x - s.cx, dy = y - s.cy, dz = z - s.cz;
+    return s.amp * fast_exp(-((dx * dx + dy * dy) + dz * dz) * s.inv2s2);
+  }
   S q = S(0);
+#pragma unroll 1
   for (int k = 0; k < g.n_gauss; ++k) {
     const SourceT<S> &s = g.src[k];
     const S dx = x - s.cx, dy = y - s.cy, dz = z - s.cz;
     const S r2 = (dx * dx + dy * dy) + dz * dz;
     q += s.amp * fast_exp(-r2 * s.inv2s2);
   }
+#pragma unroll 1
   for (int k = g.n_gauss; k < g.n_src; ++k) {
     const SourceT<S> &s = g.src[k];
     const S dx = x - s.cx, dy = y - s.cy, dz = z - s.cz;
@@ -537,8 +544,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
     }
 #pragma unroll
     for (int u = 0; u < UN; ++u) {
-      const int loc = base + u * kTileThreads;
-      if (loc >= nfree) continue;
+      // straight-line body for every lane (index clamped), predicated store
+      const bool ok = base + u * kTileThreads < nfree;
+      const int loc = ok ? base + u * kTileThreads : 0;
       const int n = n0 + loc;
       const S x = sT[loc].t;
       S Fsum;
@@ -566,8 +574,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 :
         rate += g.robin_hAT[rb] - g.robin_hA[rb] * x;
       }
       const S xn = x + fast_div(g.dt * rate, cap);
-      g.Tout[n] = xn;
-      bad |= !(fabs(xn) <= g.runaway_limit);  // also catches NaN
+      if (ok) {
+        g.Tout[n] = xn;
+        bad |= !(fabs(xn) <= g.runaway_limit);  // also catches NaN
+      }
     }
   }
   if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) s_bad = 1;

@@ -242,6 +242,14 @@ TiledState<float> &tstate<float>(fh_engine *e) { return *e->tf; }
 template <>
 TiledState<double> &tstate<double>(fh_engine *e) { return *e->tdd; }
 
+// Default tile size (nodes per part), from scripts/sweep.py on B200: fp32 hex
+// meshes 1536 (cfg4, cfg5), tet meshes 768 (~6 tets per node: the same slots
+// per tile at half the nodes; cfg3), fp64 768.
+int default_part_nodes(int precision, int64_t n_tet, int64_t n_hex) {
+  if (precision != 32) return 768;
+  return n_tet > n_hex ? 768 : 1536;
+}
+
 // Tiled kernels: a one-knot curve becomes the two-knot curve (y0, y0) with
 // slope 0 (same values everywhere).  Returns 1 when every curve of every
 // material then has exactly two knots (branch-free interpolation kernels).
@@ -391,7 +399,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   pin.tets = mesh.tets;
   pin.hexes = mesh.hexes;
   pin.node_class = cls.data();
-  pin.target_part_nodes = o.part_nodes > 0 ? o.part_nodes : (sizeof(S) == 4 ? 1536 : 768);
+  pin.target_part_nodes = o.part_nodes > 0 ? o.part_nodes : default_part_nodes(sizeof(S) == 4 ? 32 : 64, e->n_tet, e->n_hex);
   // small meshes: shrink the tiles so that at least ~2 CTAs per SM exist (latency-bound regime)
   if (o.part_nodes <= 0 && V / pin.target_part_nodes < 2 * 148)
     pin.target_part_nodes = (int)std::max<int64_t>(96, V / (2 * 148));
@@ -1606,7 +1614,7 @@ int fh_plan_create(const fh_mesh *mesh, const fh_boundary *bnd, const fh_options
   pin.tets = mesh->tets;
   pin.hexes = mesh->hexes;
   pin.node_class = cls.data();
-  pin.target_part_nodes = opts->part_nodes > 0 ? opts->part_nodes : (opts->precision == 32 ? 1536 : 768);
+  pin.target_part_nodes = opts->part_nodes > 0 ? opts->part_nodes : default_part_nodes(opts->precision, mesh->n_tets, mesh->n_hexes);
   pin.batch = kBatch;
   // layout tuning knobs (scripts/sweep.py): hex colour order, first-touch node order
   if (const char *env = getenv("FH_HEX_COLOR")) pin.hex_color = atoi(env);

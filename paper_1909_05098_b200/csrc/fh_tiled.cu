@@ -32,6 +32,10 @@ constexpr unsigned long long kNone = ~0ull;
 #define FH_MIN_BLOCKS_F32 4
 #endif
 constexpr int kMinBlocksF32 = FH_MIN_BLOCKS_F32;
+#ifndef FH_MIN_BLOCKS_TET
+#define FH_MIN_BLOCKS_TET 4
+#endif
+constexpr int kMinBlocksTet = FH_MIN_BLOCKS_TET;  // tet-only fp32 kernels: smaller tiles, more CTAs
 // global loads kept in flight per thread in the staging and node-update loops
 #ifndef FH_STAGE_UNROLL
 #define FH_STAGE_UNROLL 8
@@ -364,7 +368,8 @@ __device__ __forceinline__ void accumulate(S *acc, const uint16_t (&nd)[kSPT][N]
 }
 // KINDS: 0 hex-only, 1 tet-only, 2 mixed mesh (the absent kind's path is compiled out)
 template <typename S, bool TD, int MODE, int KINDS, bool LIN>
-__global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? kMinBlocksF32 : 2) k_tiled_step(const __grid_constant__ TiledArgs<S> g) {
+__global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? kMinBlocksTet : kMinBlocksF32) : 2)
+    k_tiled_step(const __grid_constant__ TiledArgs<S> g) {
   extern __shared__ __align__(128) unsigned char smem[];
   TK<S> *sT = reinterpret_cast<TK<S> *>(smem);
   S *acc = reinterpret_cast<S *>(smem + g.smem_T);

@@ -19,6 +19,7 @@
 // HBM traffic per step: the slot stream once (duplicated halo elements
 // included), the node streams (T, v, [q, xyz]) once, T' once, halo T from L2.
 #include <cstdio>
+#include <algorithm>
 
 #include "fh_tiled.cuh"
 
@@ -39,6 +40,9 @@ constexpr int kMinBlocksTet = FH_MIN_BLOCKS_TET;  // tet-only fp32 kernels: smal
 // global loads kept in flight per thread in the staging and node-update loops
 #ifndef FH_STAGE_UNROLL
 #define FH_STAGE_UNROLL 8
+#endif
+#ifndef FH_PREFETCH_NODES
+#define FH_PREFETCH_NODES 1
 #endif
 #ifndef FH_NODE_UNROLL
 #define FH_NODE_UNROLL 2
@@ -85,6 +89,20 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+// L2 prefetch of a 16-byte aligned range (no shared memory, no completion)
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+// any range: widened to 16-byte boundaries (allocations are 256-byte granular), 32 KB pieces
+__device__ __forceinline__ void prefetch_range(const void *p, size_t bytes) {
+  if (!p || bytes == 0) return;
+  uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~(uintptr_t)15;
+  for (; a < e; a += 32768) {
+    const uintptr_t n = e - a < 32768 ? e - a : 32768;
+    bulk_prefetch_l2(reinterpret_cast<const void *>(a), (uint32_t)n);
+  }
 }
 __device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -395,6 +413,12 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
     for (int q = 0; q < kStages; ++q) mbar_init(&bars[q], 1);
     fence_barrier_init();
     for (int j = 0; j < kStages && j < nb; ++j) issue_batch(g, p, j, nbt, ring + j * g.stage_bytes, &bars[j]);
+#if FH_PREFETCH_NODES
+    // the node update's per-node streams, pulled into L2 while the batches run
+    if (g.n_src) prefetch_range(g.xyzv + 4 * (size_t)n0, 4 * sizeof(S) * nfree);
+    else prefetch_range(g.vol + n0, sizeof(S) * nfree);
+    prefetch_range(g.q_ext ? g.q_ext + n0 : nullptr, sizeof(S) * nfree);
+#endif
   }
   // stage temperatures: owned range + halo list; zero accumulators
   const bool kstage = TD && g.mats.n == 1;

@@ -3,7 +3,7 @@
 # -> paper_1909_05098_b200/libfedheat_b200_NAME.so (use with FH_LIB=...); other units shared.
 set -e
 cd "$(dirname "$0")/../paper_1909_05098_b200/csrc"
-make -s
+test -f build/fh_exact.o || make -s  # shared units only; the main library is left as it is
 mkdir -p build_$1
 NV=/usr/local/cuda/bin/nvcc
 FL="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I../../include --expt-relaxed-constexpr"

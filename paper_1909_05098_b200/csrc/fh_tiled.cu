@@ -384,6 +384,26 @@ __device__ __forceinline__ void accumulate(S *acc, const uint16_t (&nd)[kSPT][N]
     }
   }
 }
+// colour phases: all corners of a slot share its colour's phase, so a thread
+// does its N read-modify-writes once, in its phase (warps are mostly one
+// colour: slots are colour-sorted)
+static_assert(kSPT == 1, "accumulate_colored handles one slot per thread");
+template <typename S, int N>
+__device__ __forceinline__ void accumulate_colored(S *acc, const uint16_t (&nd)[N], const S (&c)[N], int nfree,
+                                                   bool valid, int myph, int n_phase) {
+  int loc[N];
+#pragma unroll
+  for (int a = 0; a < N; ++a) loc[a] = (valid && nd[a] < nfree) ? (int)nd[a] : -1;
+  for (int ph = 0; ph < n_phase; ++ph) {
+    if (myph == ph) {
+#pragma unroll
+      for (int a = 0; a < N; ++a)
+        if (loc[a] >= 0) acc[loc[a]] -= c[a];
+    }
+    __syncthreads();
+  }
+}
+
 // KINDS: 0 hex-only, 1 tet-only, 2 mixed mesh (the absent kind's path is compiled out)
 template <typename S, bool TD, int MODE, int KINDS, bool LIN>
 __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? kMinBlocksTet : kMinBlocksF32) : 2)
@@ -498,9 +518,11 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
           rk[q][0] = w & 0xff; rk[q][1] = (w >> 8) & 0xff; rk[q][2] = (w >> 16) & 0xff; rk[q][3] = w >> 24;
         }
       }
-      accumulate<S, 4, kRanked>(acc, nd, c, nfree, valid, rk,
-                                g.tet_phase ? (int)g.tet_bnph[(t_start + b * kBatch) / kBatch]
-                                            : g.max_phase_tet);
+      if (g.tet_phase)
+        accumulate_colored<S, 4>(acc, nd[0], c[0], nfree, valid[0], rk[0][0],
+                                 (int)g.tet_bnph[(t_start + b * kBatch) / kBatch]);
+      else
+        accumulate<S, 4, kRanked>(acc, nd, c, nfree, valid, rk, g.max_phase_tet);
     } else {
       uint16_t nd[kSPT][8];
       S c[kSPT][8];
@@ -534,8 +556,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         }
       }
       if (MODE == kColored)
-        accumulate<S, 8, kRanked>(acc, nd, c, nfree, valid, rk,
-                                  g.hex_bnph[(h_start + b * kBatch) / kBatch]);
+        accumulate_colored<S, 8>(acc, nd[0], c[0], nfree, valid[0], rk[0][0],
+                                 (int)g.hex_bnph[(h_start + b * kBatch) / kBatch]);
       else
         accumulate<S, 8, MODE>(acc, nd, c, nfree, valid, rk, g.max_phase_hex);
     }

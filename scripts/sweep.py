@@ -23,11 +23,13 @@ ap.add_argument("--parts", default="768,1024")
 ap.add_argument("--modes", default="1,2")
 ap.add_argument("--stages", default="2,3")
 ap.add_argument("--steps", type=int, default=50)
+ap.add_argument("--check", action="store_true", help="compare each variant's field with the first one's")
 args = ap.parse_args()
 
 prob = bench.make_problem(args.config, args.divisions, args.precision)
 peak, _ = bench.peaks()
 t0 = time.time()
+ref = None
 for pn in [int(x) for x in args.parts.split(",")]:
     for mode in [int(x) for x in args.modes.split(",")]:
         for stg in [int(x) for x in args.stages.split(",")]:
@@ -46,7 +48,14 @@ for pn in [int(x) for x in args.parts.split(",")]:
             ms = el.value / args.steps
             lay = eng.layout()
             frac = lay["canonical_bytes"] / (ms / 1e3) / 1e9 / peak
-            print(json.dumps({"part_nodes": pn, "mode": mode, "stages": stg, "ms": round(ms, 4),
-                              "frac": round(frac, 4), "parts": lay["n_parts"], "slots": lay["n_slots"]}), flush=True)
+            rec = {"part_nodes": pn, "mode": mode, "stages": stg, "ms": round(ms, 4),
+                   "frac": round(frac, 4), "parts": lay["n_parts"], "slots": lay["n_slots"]}
+            if args.check:
+                T = eng.temperature()
+                if ref is None:
+                    ref = T
+                rec["max_rel_diff_vs_first"] = float(np.max(np.abs(T - ref) / np.maximum(np.abs(ref), 1e-30)))
+                rec["max_abs_diff_vs_first"] = float(np.max(np.abs(T - ref)))
+            print(json.dumps(rec), flush=True)
             del eng
 print("sweep wall", time.time() - t0)

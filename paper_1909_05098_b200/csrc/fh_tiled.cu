@@ -19,6 +19,7 @@
 // HBM traffic per step: the slot stream once (duplicated halo elements
 // included), the node streams (T, v, [q, xyz]) once, T' once, halo T from L2.
 #include <cstdio>
+#include <type_traits>
 #include <algorithm>
 
 #include "fh_tiled.cuh"
@@ -34,7 +35,7 @@ constexpr unsigned long long kNone = ~0ull;
 #endif
 constexpr int kMinBlocksF32 = FH_MIN_BLOCKS_F32;
 #ifndef FH_MIN_BLOCKS_TET
-#define FH_MIN_BLOCKS_TET 4
+#define FH_MIN_BLOCKS_TET 5
 #endif
 constexpr int kMinBlocksTet = FH_MIN_BLOCKS_TET;  // tet-only fp32 kernels: smaller tiles, more CTAs
 // global loads kept in flight per thread in the staging and node-update loops
@@ -573,64 +574,82 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   }
   __syncthreads();
 
-  // lumped nodal update of the owned free nodes
+  // lumped nodal update of the owned free nodes.  The per-tile uniform
+  // decisions (material lookup, source kinds, Robin rows) pick one of three
+  // loop bodies, so the common ones are branch-free and the UN nodes of a
+  // round interleave: 0 general, 1 single material / no dynamic source / no
+  // Robin row in the tile, 2 the same with exactly one Gaussian source.
   bool bad = false;
   const int rstart = g.part_robin_start[p];
   constexpr int UN = FH_NODE_UNROLL;  // nodes per thread per round: their global loads are issued together
-  for (int base = tid; base < nfree; base += UN * kTileThreads) {
-    S v[UN], q[UN], cf[UN], kf[UN], px[UN], py[UN], pz[UN];
+  auto node_loop = [&](auto kind_tag) {
+    constexpr int KIND = decltype(kind_tag)::value;
+    for (int base = tid; base < nfree; base += UN * kTileThreads) {
+      S v[UN], q[UN], cf[UN], kf[UN], px[UN], py[UN], pz[UN];
 #pragma unroll
-    for (int u = 0; u < UN; ++u) {
-      const int loc = base + u * kTileThreads;
-      const bool ok = loc < nfree;
-      const int n = n0 + (ok ? loc : 0);
-      q[u] = g.q_ext ? __ldg(g.q_ext + n) : S(0);
-      cf[u] = TD ? S(0) : __ldg(g.cap_frozen + n);
-      kf[u] = (!TD && g.kb_frozen) ? __ldg(g.kb_frozen + n) : S(0);
-      if (g.n_src) {  // packed (x, y, z, v): one vector load per node
-        load_xyzv(g.xyzv + 4 * (size_t)n, px[u], py[u], pz[u], v[u]);
-      } else {
-        v[u] = __ldg(g.vol + n);
+      for (int u = 0; u < UN; ++u) {
+        const int loc = base + u * kTileThreads;
+        const bool ok = loc < nfree;
+        const int n = n0 + (ok ? loc : 0);
+        q[u] = g.q_ext ? __ldg(g.q_ext + n) : S(0);
+        cf[u] = TD ? S(0) : __ldg(g.cap_frozen + n);
+        kf[u] = (!TD && g.kb_frozen) ? __ldg(g.kb_frozen + n) : S(0);
+        if (KIND == 2 || (KIND == 0 && g.n_src)) {  // packed (x, y, z, v): one vector load per node
+          load_xyzv(g.xyzv + 4 * (size_t)n, px[u], py[u], pz[u], v[u]);
+        } else {
+          v[u] = __ldg(g.vol + n);
+          px[u] = py[u] = pz[u] = S(0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UN; ++u) {
+        // straight-line body for every lane (index clamped), predicated store
+        const bool ok = base + u * kTileThreads < nfree;
+        const int loc = ok ? base + u * kTileThreads : 0;
+        const int n = n0 + loc;
+        const S x = sT[loc].t;
+        S Fsum;
+        if (MODE == kCornerSlot) {  // corner slots summed in fixed corner order: deterministic
+          Fsum = ((acc[loc] + acc[nfree + loc]) + (acc[2 * nfree + loc] + acc[3 * nfree + loc])) +
+                 ((acc[4 * nfree + loc] + acc[5 * nfree + loc]) + (acc[6 * nfree + loc] + acc[7 * nfree + loc]));
+        } else if (MODE == kCornerPhase2) {
+          Fsum = acc[loc] + acc[nfree + loc];
+        } else {
+          Fsum = acc[loc];
+        }
+        S rate;
+        S cap;
+        if (KIND != 0 || !g.node_region)  // single material: curve parameters are uniform operands
+          rate = node_rate<S, TD, LIN>(g.mats.m[0], x, Fsum, v[u], q[u], cf[u], kf[u], cap);
+        else
+          rate = node_rate<S, TD, LIN>(g.mats.m[g.node_region[n]], x, Fsum, v[u], q[u], cf[u], kf[u], cap);
+        if (KIND == 2) {
+          const SourceT<S> &sr = g.src[0];
+          const S dx = px[u] - sr.cx, dy = py[u] - sr.cy, dz = pz[u] - sr.cz;
+          rate += sr.amp * fast_exp(-((dx * dx + dy * dy) + dz * dz) * sr.inv2s2) * v[u];
+        } else if (KIND == 0 && g.n_src) {
+          const S xyz[3] = {px[u], py[u], pz[u]};
+          rate += sources_at(g, xyz) * v[u];
+        }
+        if (KIND == 0 && loc >= rstart) {
+          const int rb = g.part_robin_base[p] + (loc - rstart);
+          rate += g.robin_hAT[rb] - g.robin_hA[rb] * x;
+        }
+        const S xn = x + fast_div(g.dt * rate, cap);
+        if (ok) {
+          g.Tout[n] = xn;
+          bad |= !(fabs(xn) <= g.runaway_limit);  // also catches NaN
+        }
       }
     }
-#pragma unroll
-    for (int u = 0; u < UN; ++u) {
-      // straight-line body for every lane (index clamped), predicated store
-      const bool ok = base + u * kTileThreads < nfree;
-      const int loc = ok ? base + u * kTileThreads : 0;
-      const int n = n0 + loc;
-      const S x = sT[loc].t;
-      S Fsum;
-      if (MODE == kCornerSlot) {  // corner slots summed in fixed corner order: deterministic
-        Fsum = ((acc[loc] + acc[nfree + loc]) + (acc[2 * nfree + loc] + acc[3 * nfree + loc])) +
-               ((acc[4 * nfree + loc] + acc[5 * nfree + loc]) + (acc[6 * nfree + loc] + acc[7 * nfree + loc]));
-      } else if (MODE == kCornerPhase2) {
-        Fsum = acc[loc] + acc[nfree + loc];
-      } else {
-        Fsum = acc[loc];
-      }
-      S rate;
-      S cap;
-      // single material: curve parameters are uniform kernel-parameter operands
-      if (!g.node_region)
-        rate = node_rate<S, TD, LIN>(g.mats.m[0], x, Fsum, v[u], q[u], cf[u], kf[u], cap);
-      else
-        rate = node_rate<S, TD, LIN>(g.mats.m[g.node_region[n]], x, Fsum, v[u], q[u], cf[u], kf[u], cap);
-      if (g.n_src) {
-        const S xyz[3] = {px[u], py[u], pz[u]};
-        rate += sources_at(g, xyz) * v[u];
-      }
-      if (loc >= rstart) {
-        const int rb = g.part_robin_base[p] + (loc - rstart);
-        rate += g.robin_hAT[rb] - g.robin_hA[rb] * x;
-      }
-      const S xn = x + fast_div(g.dt * rate, cap);
-      if (ok) {
-        g.Tout[n] = xn;
-        bad |= !(fabs(xn) <= g.runaway_limit);  // also catches NaN
-      }
-    }
-  }
+  };
+  const bool simple = !g.node_region && rstart >= nfree;
+  if (simple && g.n_src == 0)
+    node_loop(std::integral_constant<int, 1>{});
+  else if (simple && g.n_src == 1 && g.n_gauss == 1)
+    node_loop(std::integral_constant<int, 2>{});
+  else
+    node_loop(std::integral_constant<int, 0>{});
   if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) s_bad = 1;
   __syncthreads();
   if (tid == 0 && s_bad) atomicMin(&g.flag->step, g.step_no);

@@ -614,9 +614,11 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.smem_acc = (int)al(sizeof(S) * rows * ((size_t)std::max(1, P.max_part_free) + 1));
   int stage = 0;
   if (e->n_tet)
-    stage = std::max(stage, StageBytes<S>(4, st->tet_kf.p || !e->td, tet_mode == kModeRanked, tet_mode == kModeColored));
+    stage = std::max(stage, StageBytes<S>(4, st->tet_kf.p || !e->td, tet_mode == kModeRanked, tet_mode == kModeColored,
+                                          st->tet_region.p != nullptr));
   if (e->n_hex)
-    stage = std::max(stage, StageBytes<S>(8, st->hex_kf.p || !e->td, mode == kModeRanked, mode == kModeColored));
+    stage = std::max(stage, StageBytes<S>(8, st->hex_kf.p || !e->td, mode == kModeRanked, mode == kModeColored,
+                                          st->hex_region.p != nullptr));
   g.stage_bytes = (int)al(stage);
   st->smem = (size_t)g.smem_T + g.smem_acc + (size_t)g.n_stages * g.stage_bytes;
   if (st->smem > 220 * 1024) fail(FH_ERR_CONFIG, "tile too large for shared memory; lower part_nodes");

@@ -111,12 +111,13 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // stage layout for one batch of B slots of a kind with N corners
 template <typename S>
 struct StageLayout {
-  int conn, G, kf, rank, phase;
-  __host__ __device__ StageLayout(int N, bool has_kf, bool has_rank) {
+  int conn, G, kf, region, rank, phase;
+  __host__ __device__ StageLayout(int N, bool has_kf, bool has_rank, bool has_region) {
     conn = 0;
     G = kBatch * N * 2;
     kf = G + 6 * kBatch * (int)sizeof(S);
-    rank = kf + (has_kf ? kBatch * (int)sizeof(S) : 0);
+    region = kf + (has_kf ? kBatch * (int)sizeof(S) : 0);  // material byte per slot (several materials only)
+    rank = region + (has_region ? kBatch : 0);
     phase = rank + (has_rank ? kBatch * N : 0);  // colored mode only (no rank block then)
   }
 };
@@ -211,14 +212,17 @@ __device__ void issue_batch(const TiledArgs<S> &g, int p, int j, int nbt, unsign
   const S *kf = tet ? g.tet_kf : g.hex_kf;
   const uint8_t *rank = tet ? g.tet_rank : g.hex_rank;
   const uint8_t *phase = tet ? g.tet_phase : g.hex_phase;
-  const StageLayout<S> L(N, kf != nullptr, rank != nullptr);
+  const uint8_t *region = tet ? g.tet_region : g.hex_region;
+  const StageLayout<S> L(N, kf != nullptr, rank != nullptr, region != nullptr);
   const int kp = (k + 15) & ~15;  // bulk copies move multiples of 16 bytes
   uint32_t bytes = (uint32_t)(kr * N * 2 + 6 * kr * sizeof(S));
   if (kf) bytes += kr * sizeof(S);
   if (rank) bytes += kr * N;
   if (phase) bytes += kp;
+  if (region) bytes += kp;
   mbar_expect_tx(bar, bytes);
   if (phase) bulk_g2s(stage + L.phase, phase + s0, kp, bar);
+  if (region) bulk_g2s(stage + L.region, region + s0, kp, bar);
   bulk_g2s(stage + L.conn, conn + (size_t)N * s0, kr * N * 2, bar);
   const S *Gb = G + (size_t)(s0 / kBatch) * 6 * kBatch;
 #pragma unroll
@@ -232,7 +236,7 @@ __device__ void issue_batch(const TiledArgs<S> &g, int p, int j, int nbt, unsign
 template <typename S, bool TD, bool LIN>
 __device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned char *stage, const TK<S> *sT,
                                           const Curve<S> &kc, bool has_kf, int i, uint16_t nd[8], S c[8]) {
-  const StageLayout<S> L(8, has_kf, g.hex_rank != nullptr);
+  const StageLayout<S> L(8, has_kf, g.hex_rank != nullptr, g.hex_region != nullptr);
   const uint4 w = reinterpret_cast<const uint4 *>(stage + L.conn)[i];
   nd[0] = w.x & 0xffff; nd[1] = w.x >> 16; nd[2] = w.y & 0xffff; nd[3] = w.y >> 16;
   nd[4] = w.z & 0xffff; nd[5] = w.z >> 16; nd[6] = w.w & 0xffff; nd[7] = w.w >> 16;
@@ -272,7 +276,7 @@ __device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned 
 template <typename S, bool TD, bool LIN>
 __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned char *stage, const TK<S> *sT,
                                           const Curve<S> &kc, bool has_kf, int i, uint16_t nd[4], S c[4]) {
-  const StageLayout<S> L(4, has_kf, g.tet_rank != nullptr);
+  const StageLayout<S> L(4, has_kf, g.tet_rank != nullptr, g.tet_region != nullptr);
   const uint2 w = reinterpret_cast<const uint2 *>(stage + L.conn)[i];
   nd[0] = w.x & 0xffff; nd[1] = w.x >> 16; nd[2] = w.y & 0xffff; nd[3] = w.y >> 16;
   S T[4], K[4];
@@ -498,7 +502,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       for (int q = 0; q < kSPT; ++q) {
         const int i = q * kTileThreads + tid;
         const int s = t_start + b * kBatch + i;
-        const Curve<S> &kc = g.mats.m[(g.tet_region && valid[q]) ? g.tet_region[s] : 0].k;
+        const Curve<S> &kc =
+            g.mats.m[(g.tet_region && valid[q])
+                         ? stage[StageLayout<S>(4, g.tet_kf != nullptr, g.tet_rank != nullptr, true).region + i]
+                         : 0].k;
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
           nd[q][a] = 0;
@@ -509,12 +516,12 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         // tets are never corner-unique: colour phases (phase byte per slot) or,
         // if the colouring overflowed, ranked phases (rank byte per corner)
         if (valid[q] && g.tet_phase) {
-          const StageLayout<S> L(4, g.tet_kf != nullptr, false);
+          const StageLayout<S> L(4, g.tet_kf != nullptr, false, g.tet_region != nullptr);
           const uint8_t ph = stage[L.phase + i];
 #pragma unroll
           for (int a = 0; a < 4; ++a) rk[q][a] = ph;
         } else if (valid[q]) {
-          const StageLayout<S> L(4, g.tet_kf != nullptr, true);
+          const StageLayout<S> L(4, g.tet_kf != nullptr, true, g.tet_region != nullptr);
           const uint32_t w = reinterpret_cast<const uint32_t *>(stage + L.rank)[i];
           rk[q][0] = w & 0xff; rk[q][1] = (w >> 8) & 0xff; rk[q][2] = (w >> 16) & 0xff; rk[q][3] = w >> 24;
         }
@@ -532,7 +539,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       for (int q = 0; q < kSPT; ++q) {
         const int i = q * kTileThreads + tid;
         const int s = h_start + b * kBatch + i;
-        const Curve<S> &kc = g.mats.m[(g.hex_region && valid[q]) ? g.hex_region[s] : 0].k;
+        const Curve<S> &kc =
+            g.mats.m[(g.hex_region && valid[q])
+                         ? stage[StageLayout<S>(8, g.hex_kf != nullptr, g.hex_rank != nullptr, true).region + i]
+                         : 0].k;
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
           nd[q][a] = 0;
@@ -541,7 +551,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         }
         if (valid[q]) hex_loads<S, TD, LIN>(g, stage, sT, kc, g.hex_kf != nullptr, i, nd[q], c[q]);
         if (MODE == kRanked && valid[q]) {
-          const StageLayout<S> L(8, g.hex_kf != nullptr, true);
+          const StageLayout<S> L(8, g.hex_kf != nullptr, true, g.hex_region != nullptr);
           const uint2 w = reinterpret_cast<const uint2 *>(stage + L.rank)[i];
 #pragma unroll
           for (int a = 0; a < 4; ++a) {
@@ -550,7 +560,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
           }
         }
         if (MODE == kColored && valid[q]) {
-          const StageLayout<S> L(8, g.hex_kf != nullptr, false);
+          const StageLayout<S> L(8, g.hex_kf != nullptr, false, g.hex_region != nullptr);
           const uint8_t ph = stage[L.phase + i];
 #pragma unroll
           for (int a = 0; a < 8; ++a) rk[q][a] = ph;

@@ -62,11 +62,12 @@ struct TiledArgs {
   unsigned long long step_no;
 };
 
-// bytes of one staged batch: conn16 [B][N] | G [6][B] | kf [B] | rank [B][N] | phase [B]
+// bytes of one staged batch: conn16 [B][N] | G [6][B] | kf [B] | region [B] | rank [B][N] | phase [B]
 template <typename S>
-inline int StageBytes(int N, bool has_kf, bool has_rank, bool has_phase = false) {
+inline int StageBytes(int N, bool has_kf, bool has_rank, bool has_phase = false, bool has_region = false) {
   int b = kBatch * N * 2 + 6 * kBatch * (int)sizeof(S);
   if (has_kf) b += kBatch * (int)sizeof(S);
+  if (has_region) b += kBatch;
   if (has_rank) b += kBatch * N;
   if (has_phase) b += kBatch;
   return (b + 15) & ~15;

@@ -113,8 +113,11 @@ __global__ void k_pack_slots(const int32_t *__restrict__ slot_elem, int64_t n, c
   const int64_t e = slot_elem[s];
   // G in batch-major SoA: [s / B][component][s % B]
   const int64_t base = (s / kBatch) * 6 * kBatch + (s % kBatch);
+  // temperature-dependent runs fold the conductivity factor into G (no kf
+  // stream: out_kf == nullptr); frozen runs keep it for the freeze
+  const double f = (kf && !out_kf && e >= 0) ? kf[e] : 1.0;
 #pragma unroll
-  for (int k = 0; k < 6; ++k) out_G[base + k * kBatch] = e >= 0 ? (S)(G[6 * e + k] * scale) : S(0);
+  for (int k = 0; k < 6; ++k) out_G[base + k * kBatch] = e >= 0 ? (S)(G[6 * e + k] * scale * f) : S(0);
   if (out_kf) out_kf[s] = e >= 0 ? (S)kf[e] : S(1);
   if (out_region) out_region[s] = e >= 0 ? (uint8_t)region[e] : 0;
 }
@@ -493,7 +496,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   st->tet_G.alloc(6 * nts);
   st->hex_G.alloc(6 * nhs);
   const bool regions = o.n_materials > 1 && o.element_region;
-  if (e->kfactor.p) {
+  if (e->kfactor.p && !e->td) {  // TD: folded into G by k_pack_slots
     st->tet_kf.alloc(nts);
     st->hex_kf.alloc(nhs);
   }
@@ -1332,14 +1335,24 @@ int fh_get_layout(fh_engine *e, fh_layout *out) {
     int64_t owned = 0;
     for (int p = 0; p < P.n_parts; ++p) owned += P.part_n_free[p];
     out->n_nodes_owned = owned;
-    int64_t b = nts * (16 + 6 * s) + nhs * (32 + 6 * s);
-    if (e->kfactor.p || !e->td) b += (nts + nhs) * s;
-    if (!P.corner_unique) b += nts * 4 + nhs * 8;
+    // slot streams as stored: 16-bit connectivity, G (conductivity factor
+    // folded in when temperature-dependent), frozen kbar (TI), material byte,
+    // per-corner rank (ranked mode) or per-slot phase (colour mode)
+    const bool regions = (e->tf && e->tf->hex_region.p) || (e->tf && e->tf->tet_region.p) ||
+                         (e->tdd && e->tdd->hex_region.p) || (e->tdd && e->tdd->tet_region.p);
+    const int hex_mode = e->tf ? e->tf->mode : (e->tdd ? e->tdd->mode : 0);
+    int64_t b = nts * (8 + 6 * s) + nhs * (16 + 6 * s);
+    if (!e->td) b += (nts + nhs) * s;
+    if (regions) b += nts + nhs;
+    if (P.colored_ok) b += nts; else b += nts * 4;
+    if (hex_mode == kModeRanked) b += nhs * 8;
+    if (hex_mode == kModeColored) b += nhs;
     int64_t node_streams = 3 * s;  // T read, T' write, v
     if (!e->td) node_streams += s;  // frozen capacity
     if (!e->q_static.empty() || !e->load_power.empty()) node_streams += s;
     if (!e->sources.empty()) node_streams += 3 * s;
     b += owned * node_streams;
+    b += (int64_t)P.halo_nodes.size() * s;  // halo temperatures (each tile stages its own)
     out->step_bytes = b;
   }
   FH_API_END

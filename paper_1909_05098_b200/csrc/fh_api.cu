@@ -455,7 +455,11 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   st->part_tet_count.upload(P.part_tet_count, s);
   st->part_hex_count.upload(P.part_hex_count, s);
   st->part_halo_start.upload(P.part_halo_start, s);
-  st->halo_nodes.upload(P.halo_nodes, s);
+  {  // +4 entries: the kernel bulk-copies each tile's list widened to 16-byte boundaries
+    std::vector<int32_t> hn(P.halo_nodes);
+    hn.resize(hn.size() + 4, 0);
+    st->halo_nodes.upload(hn, s);
+  }
   st->tet_conn16.upload(P.tet_conn16, s);
   st->hex_conn16.upload(P.hex_conn16, s);
   if (!e->td) {  // the TI freeze kernel works on global ids
@@ -615,6 +619,11 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   // +1: the trash slot of the corner-phase accumulation
   const int rows = st->mode == kModeCornerSlot ? 8 : (st->mode == kModeCornerPhase2 ? 2 : 1);
   g.smem_acc = (int)al(sizeof(S) * rows * ((size_t)std::max(1, P.max_part_free) + 1));
+  {  // the accumulator region first holds the tile's halo id list (bulk copy)
+    int max_halo = 0;
+    for (int q = 0; q < P.n_parts; ++q) max_halo = std::max(max_halo, P.part_halo_start[q + 1] - P.part_halo_start[q]);
+    g.smem_acc = std::max(g.smem_acc, (int)al(4 * ((size_t)max_halo + 8)));
+  }
   int stage = 0;
   if (e->n_tet)
     stage = std::max(stage, StageBytes<S>(4, st->tet_kf.p || !e->td, tet_mode == kModeRanked, tet_mode == kModeColored,

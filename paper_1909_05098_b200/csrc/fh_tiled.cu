@@ -419,6 +419,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   unsigned char *ring = smem + g.smem_T + g.smem_acc;
   const int kStages = g.n_stages;
   __shared__ __align__(8) uint64_t bars[kMaxStages];
+  __shared__ __align__(8) uint64_t hbar;  // halo id list copy
   __shared__ int s_bad;
   if (g.flag->step != kNone) return;
   const int p = g.part_list ? g.part_list[g.part_begin + blockIdx.x] : g.part_begin + (int)blockIdx.x;
@@ -432,11 +433,24 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   const int nbt = (t_cnt + kBatch - 1) / kBatch;
   const int nbh = (g.part_hex_count[p] + kBatch - 1) / kBatch;
   const int nb = nbt + nbh;
+  // the tile's halo id list is bulk-copied into the (not yet used) accumulator
+  // region first thing, so the halo gather waits one round trip, not two.
+  // The copy is widened to 16-byte boundaries (the list is padded at its end).
+  const int h0 = g.part_halo_start[p], nh = g.part_halo_start[p + 1] - h0;
+  const int hs = h0 & ~3, hoff = h0 - hs;
+  int32_t *s_ids = reinterpret_cast<int32_t *>(acc);
   if (tid == 0) {
     s_bad = 0;
 #pragma unroll
     for (int q = 0; q < kStages; ++q) mbar_init(&bars[q], 1);
+    mbar_init(&hbar, 1);
     fence_barrier_init();
+  }
+  __syncthreads();  // the mbarriers are initialised before anyone waits on them
+  if (tid == 0) {
+    const uint32_t hbytes = (uint32_t)((((h0 + nh + 3) & ~3) - hs) * 4);
+    mbar_expect_tx(&hbar, hbytes);
+    if (hbytes) bulk_g2s(s_ids, g.halo_nodes + hs, hbytes, &hbar);
     for (int j = 0; j < kStages && j < nb; ++j) issue_batch(g, p, j, nbt, ring + j * g.stage_bytes, &bars[j]);
 #if FH_PREFETCH_NODES
     // the node update's per-node streams, pulled into L2 while the batches run
@@ -462,13 +476,13 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       if (i < nn) sT[i] = TK<S>{x[u], kstage ? ip<LIN>(k0, x[u]) : S(0)};
     }
   }
-  const int h0 = g.part_halo_start[p], nh = g.part_halo_start[p + 1] - h0;
+  mbar_wait(&hbar, 0);
   for (int base = tid; base < nh; base += U * kTileThreads) {
     int id[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = base + u * kTileThreads;
-      id[u] = i < nh ? __ldg(g.halo_nodes + h0 + i) : 0;
+      id[u] = i < nh ? s_ids[hoff + i] : 0;
     }
     S x[U];
 #pragma unroll
@@ -479,6 +493,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       if (i < nh) sT[nn + i] = TK<S>{x[u], kstage ? ip<LIN>(k0, x[u]) : S(0)};
     }
   }
+  __syncthreads();  // every halo id has been read: the accumulators may be zeroed
   for (int i = tid; i < (MODE == kCornerSlot ? 8 : (MODE == kCornerPhase2 ? 2 : 1)) * nfree; i += kTileThreads)
     acc[i] = S(0);
   __syncthreads();

@@ -105,14 +105,14 @@ __global__ void k_xyzv_to_new(const double *__restrict__ xyz, const int64_t *__r
 
 template <typename S>
 __global__ void k_pack_slots(const int32_t *__restrict__ slot_elem, int64_t n, const double *__restrict__ G,
-                             double scale, S *__restrict__ out_G, const double *__restrict__ kf,
+                             double scale, S *__restrict__ out_G, int rec_elems, int g_off, const double *__restrict__ kf,
                              S *__restrict__ out_kf, const int32_t *__restrict__ region,
                              uint8_t *__restrict__ out_region) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= n) return;
   const int64_t e = slot_elem[s];
-  // G in batch-major SoA: [s / B][component][s % B]
-  const int64_t base = (s / kBatch) * 6 * kBatch + (s % kBatch);
+  // G rows of the batch record: record s / B, element offset g_off, [component][s % B]
+  const int64_t base = (s / kBatch) * rec_elems + g_off + (s % kBatch);
   // temperature-dependent runs fold the conductivity factor into G (no kf
   // stream: out_kf == nullptr); frozen runs keep it for the freeze
   const double f = (kf && !out_kf && e >= 0) ? kf[e] : 1.0;
@@ -131,9 +131,9 @@ struct TiledState {
   DBuf<int32_t> part_node_start, part_n_free, part_robin_start, part_robin_base, part_tet_start, part_hex_start;
   DBuf<int32_t> part_tet_count, part_hex_count, part_halo_start, halo_nodes;
   DBuf<int32_t> part_list;
-  DBuf<uint16_t> tet_conn16, hex_conn16;
+  DBuf<unsigned char> tet_rec, hex_rec;  // per-batch [conn16 | G] records (RecBytes)
   DBuf<int32_t> tet_conn, hex_conn, tet_slot_elem, hex_slot_elem;
-  DBuf<S> tet_G, hex_G, tet_kf, hex_kf, tet_kbar, hex_kbar;
+  DBuf<S> tet_kf, hex_kf, tet_kbar, hex_kbar;
   DBuf<uint8_t> tet_rank, hex_rank, tet_region, hex_region, node_region;
   DBuf<uint8_t> tet_phase, hex_phase, tet_bnph, hex_bnph;
   DBuf<S> T[2], vol, cap, kb, q_ext, xyz, robin_hA, robin_hAT;
@@ -460,8 +460,6 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     hn.resize(hn.size() + 4, 0);
     st->halo_nodes.upload(hn, s);
   }
-  st->tet_conn16.upload(P.tet_conn16, s);
-  st->hex_conn16.upload(P.hex_conn16, s);
   if (!e->td) {  // the TI freeze kernel works on global ids
     st->tet_conn.upload(P.tet_conn, s);
     st->hex_conn.upload(P.hex_conn, s);
@@ -497,8 +495,16 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     st->tet_bnph.upload(P.tet_batch_nph, s);
   }
   const int64_t nts = (int64_t)P.tet_slot_elem.size(), nhs = (int64_t)P.hex_slot_elem.size();
-  st->tet_G.alloc(6 * nts);
-  st->hex_G.alloc(6 * nhs);
+  // batch records: the 16-bit connectivity goes in by a pitched copy, G by k_pack_slots
+  auto make_rec = [&](DBuf<unsigned char> &rec, const std::vector<uint16_t> &conn16, int64_t n, int N) {
+    const int64_t nbat = n / kBatch;  // slot ranges are batch-padded
+    rec.alloc((size_t)nbat * RecBytes<S>(N));
+    if (nbat)
+      FH_CUDA(cudaMemcpy2DAsync(rec.p, RecBytes<S>(N), conn16.data(), (size_t)kBatch * N * 2, (size_t)kBatch * N * 2,
+                                (size_t)nbat, cudaMemcpyHostToDevice, s));
+  };
+  make_rec(st->tet_rec, P.tet_conn16, nts, 4);
+  make_rec(st->hex_rec, P.hex_conn16, nhs, 8);
   const bool regions = o.n_materials > 1 && o.element_region;
   if (e->kfactor.p && !e->td) {  // TD: folded into G by k_pack_slots
     st->tet_kf.alloc(nts);
@@ -509,11 +515,15 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     st->hex_region.alloc(nhs);
   }
   if (nts)
-    k_pack_slots<S><<<nblk(nts), kBlk, 0, s>>>(st->tet_slot_elem.p, nts, G_dev, 1.0, st->tet_G.p, e->kfactor.p,
-                                               st->tet_kf.p, e->elem_region.p, st->tet_region.p);
+    k_pack_slots<S><<<nblk(nts), kBlk, 0, s>>>(st->tet_slot_elem.p, nts, G_dev, 1.0,
+                                               reinterpret_cast<S *>(st->tet_rec.p), RecBytes<S>(4) / (int)sizeof(S),
+                                               kBatch * 4 * 2 / (int)sizeof(S), e->kfactor.p, st->tet_kf.p,
+                                               e->elem_region.p, st->tet_region.p);
   if (nhs)
-    k_pack_slots<S><<<nblk(nhs), kBlk, 0, s>>>(st->hex_slot_elem.p, nhs, G_dev, 1.0 / 64.0, st->hex_G.p,
-                                               e->kfactor.p, st->hex_kf.p, e->elem_region.p, st->hex_region.p);
+    k_pack_slots<S><<<nblk(nhs), kBlk, 0, s>>>(st->hex_slot_elem.p, nhs, G_dev, 1.0 / 64.0,
+                                               reinterpret_cast<S *>(st->hex_rec.p), RecBytes<S>(8) / (int)sizeof(S),
+                                               kBatch * 8 * 2 / (int)sizeof(S), e->kfactor.p, st->hex_kf.p,
+                                               e->elem_region.p, st->hex_region.p);
   FH_CUDA(cudaGetLastError());
   // nodal arrays in the new numbering
   st->T[0].alloc(V);
@@ -579,10 +589,8 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.part_hex_count = st->part_hex_count.p;
   g.part_halo_start = st->part_halo_start.p;
   g.halo_nodes = st->halo_nodes.p;
-  g.tet_conn16 = st->tet_conn16.p;
-  g.hex_conn16 = st->hex_conn16.p;
-  g.tet_G = st->tet_G.p;
-  g.hex_G = st->hex_G.p;
+  g.tet_rec = st->tet_rec.p;
+  g.hex_rec = st->hex_rec.p;
   g.tet_kf = st->tet_kf.p;
   g.hex_kf = st->hex_kf.p;
   g.tet_phase = st->tet_phase.p;

@@ -207,8 +207,7 @@ __device__ void issue_batch(const TiledArgs<S> &g, int p, int j, int nbt, unsign
   const int cnt = (tet ? g.part_tet_count[p] : g.part_hex_count[p]) - b * kBatch;
   const int k = cnt < kBatch ? cnt : kBatch;
   const int kr = (k + 3) & ~3;
-  const uint16_t *conn = tet ? g.tet_conn16 : g.hex_conn16;
-  const S *G = tet ? g.tet_G : g.hex_G;
+  const unsigned char *rec = (tet ? g.tet_rec : g.hex_rec) + (size_t)(s0 / kBatch) * RecBytes<S>(N);
   const S *kf = tet ? g.tet_kf : g.hex_kf;
   const uint8_t *rank = tet ? g.tet_rank : g.hex_rank;
   const uint8_t *phase = tet ? g.tet_phase : g.hex_phase;
@@ -223,11 +222,15 @@ __device__ void issue_batch(const TiledArgs<S> &g, int p, int j, int nbt, unsign
   mbar_expect_tx(bar, bytes);
   if (phase) bulk_g2s(stage + L.phase, phase + s0, kp, bar);
   if (region) bulk_g2s(stage + L.region, region + s0, kp, bar);
-  bulk_g2s(stage + L.conn, conn + (size_t)N * s0, kr * N * 2, bar);
-  const S *Gb = G + (size_t)(s0 / kBatch) * 6 * kBatch;
+  if (kr == kBatch) {  // a full batch: one copy of the whole record (conn16 + 6 G rows)
+    bulk_g2s(stage + L.conn, rec, RecBytes<S>(N), bar);
+  } else {
+    bulk_g2s(stage + L.conn, rec, kr * N * 2, bar);
+    const unsigned char *Gb = rec + kBatch * N * 2;
 #pragma unroll
-  for (int c = 0; c < 6; ++c)
-    bulk_g2s(stage + L.G + c * kBatch * sizeof(S), Gb + c * kBatch, kr * sizeof(S), bar);
+    for (int c = 0; c < 6; ++c)
+      bulk_g2s(stage + L.G + c * kBatch * sizeof(S), Gb + c * kBatch * sizeof(S), kr * sizeof(S), bar);
+  }
   if (kf) bulk_g2s(stage + L.kf, kf + s0, kr * sizeof(S), bar);
   if (rank) bulk_g2s(stage + L.rank, rank + (size_t)N * s0, kr * N, bar);
 }
@@ -702,7 +705,7 @@ void tiled_step(const TiledArgs<S> &g, int n_parts, bool td, int mode_sel, size_
 #undef FH_MODES
 #undef FH_TETONLY
   const int mode = mode_sel < 0 || mode_sel > 5 ? 0 : mode_sel;
-  const int kinds = (g.part_tet_start && g.tet_conn16 && g.hex_conn16) ? 2 : (g.hex_conn16 ? 0 : 1);
+  const int kinds = (g.tet_rec && g.hex_rec) ? 2 : (g.hex_rec ? 0 : 1);
   const int lin = g.lin ? 1 : 0;
   const K kern = table[lin][td ? 1 : 0][kinds][mode];
   static size_t configured[2][2][3][6] = {};

@@ -22,8 +22,8 @@ struct SourceT {
 
 // Slot streams of a part are stored in batches of kTileThreads slots, every
 // part's range starting on a batch boundary:
-//   conn16 [slot][N]   uint16 tile-local node index (owned | halo)
-//   G      [batch][6][B] metric tensor components (hex pre-scaled by 1/64)
+//   rec    [batch] { conn16 [B][N] uint16 tile-local node index (owned | halo),
+//                    G [6][B] metric tensor components (hex pre-scaled by 1/64) }
 //   kf     [slot]      conductivity factor (TD) or frozen kbar (TI), optional
 //   rank   [slot][N]   accumulation phase per corner (ranked mode only)
 template <typename S>
@@ -33,8 +33,8 @@ struct TiledArgs {
   const int32_t *part_node_start, *part_n_free, *part_robin_start, *part_robin_base;
   const int32_t *part_tet_start, *part_tet_count, *part_hex_start, *part_hex_count;
   const int32_t *part_halo_start, *halo_nodes;
-  const uint16_t *tet_conn16, *hex_conn16;
-  const S *tet_G, *hex_G;
+  // per-batch records [conn16 block | G block] (RecBytes), null when the kind is absent
+  const unsigned char *tet_rec, *hex_rec;
   const S *tet_kf, *hex_kf;
   const uint8_t *tet_rank, *hex_rank;  // null: corner-unique (phase == corner)
   const uint8_t *tet_phase, *hex_phase;  // colored mode: phase per slot
@@ -61,6 +61,14 @@ struct TiledArgs {
   FailFlag *flag;
   unsigned long long step_no;
 };
+
+// one batch record of the connectivity + metric stream in HBM, laid out like
+// the head of the stage: conn16 [B][N] (uint16) | G [6][B] (hex pre-scaled by
+// 1/64, conductivity factor folded in when temperature-dependent)
+template <typename S>
+constexpr int RecBytes(int N) {
+  return kBatch * N * 2 + 6 * kBatch * (int)sizeof(S);
+}
 
 // bytes of one staged batch: conn16 [B][N] | G [6][B] | kf [B] | region [B] | rank [B][N] | phase [B]
 template <typename S>

@@ -238,7 +238,7 @@ __device__ void issue_batch(const TiledArgs<S> &g, int p, int j, int nbt, unsign
 // element loads of staged slot i of the batch ------------------------------------
 template <typename S, bool TD, bool LIN>
 __device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned char *stage, const TK<S> *sT,
-                                          const Curve<S> &kc, bool has_kf, int i, uint16_t nd[8], S c[8]) {
+                                          int reg, bool has_kf, int i, uint16_t nd[8], S c[8]) {
   const StageLayout<S> L(8, has_kf, g.hex_rank != nullptr, g.hex_region != nullptr);
   const uint4 w = reinterpret_cast<const uint4 *>(stage + L.conn)[i];
   nd[0] = w.x & 0xffff; nd[1] = w.x >> 16; nd[2] = w.y & 0xffff; nd[3] = w.y >> 16;
@@ -256,11 +256,11 @@ __device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned 
   const S kf = has_kf ? reinterpret_cast<const S *>(stage + L.kf)[i] : S(1);
   S kb = kf;
   if (TD) {
-    if (g.mats.n == 1) {  // k(T) staged per node: kbar = mean of the corner values
+    if (reg == 0) {  // k(T) of material 0 staged per node: kbar = mean of the corner values
       const S sum = ((K[0] + K[1]) + (K[2] + K[3])) + ((K[4] + K[5]) + (K[6] + K[7]));
       kb = sum * S(0.125) * kf;
-    } else {
-      kb = kbar_from<LIN>(kc, T, 8, kf);
+    } else {  // other materials (rare slots): the element's own curve at each corner
+      kb = kbar_from<LIN>(g.mats.m[reg].k, T, 8, kf);
     }
   }
   // g = sum_b s_b (T_b - T_0) with the corner signs of element.py HEX_VERTEX_SIGNS
@@ -278,7 +278,7 @@ __device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned 
 
 template <typename S, bool TD, bool LIN>
 __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned char *stage, const TK<S> *sT,
-                                          const Curve<S> &kc, bool has_kf, int i, uint16_t nd[4], S c[4]) {
+                                          int reg, bool has_kf, int i, uint16_t nd[4], S c[4]) {
   const StageLayout<S> L(4, has_kf, g.tet_rank != nullptr, g.tet_region != nullptr);
   const uint2 w = reinterpret_cast<const uint2 *>(stage + L.conn)[i];
   nd[0] = w.x & 0xffff; nd[1] = w.x >> 16; nd[2] = w.y & 0xffff; nd[3] = w.y >> 16;
@@ -295,10 +295,10 @@ __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned 
   const S kf = has_kf ? reinterpret_cast<const S *>(stage + L.kf)[i] : S(1);
   S kb = kf;
   if (TD) {
-    if (g.mats.n == 1) {
+    if (reg == 0) {
       kb = ((K[0] + K[1]) + (K[2] + K[3])) * S(0.25) * kf;
     } else {
-      kb = kbar_from<LIN>(kc, T, 4, kf);
+      kb = kbar_from<LIN>(g.mats.m[reg].k, T, 4, kf);
     }
   }
   const S d1 = T[1] - T[0], d2 = T[2] - T[0], d3 = T[3] - T[0];
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
 #endif
   }
   // stage temperatures: owned range + halo list; zero accumulators
-  const bool kstage = TD && g.mats.n == 1;
+  const bool kstage = TD;  // k of material 0 (other materials interpolate per slot)
   const Curve<S> &k0 = g.mats.m[0].k;
   constexpr int U = FH_STAGE_UNROLL;  // loads in flight per thread while staging
   for (int base = tid; base < nn; base += U * kTileThreads) {
@@ -520,17 +520,16 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       for (int q = 0; q < kSPT; ++q) {
         const int i = q * kTileThreads + tid;
         const int s = t_start + b * kBatch + i;
-        const Curve<S> &kc =
-            g.mats.m[(g.tet_region && valid[q])
-                         ? stage[StageLayout<S>(4, g.tet_kf != nullptr, g.tet_rank != nullptr, true).region + i]
-                         : 0].k;
+        const int reg = (g.tet_region && valid[q])
+                            ? stage[StageLayout<S>(4, g.tet_kf != nullptr, g.tet_rank != nullptr, true).region + i]
+                            : 0;
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
           nd[q][a] = 0;
           c[q][a] = S(0);
           rk[q][a] = 0xff;
         }
-        if (valid[q]) tet_loads<S, TD, LIN>(g, stage, sT, kc, g.tet_kf != nullptr, i, nd[q], c[q]);
+        if (valid[q]) tet_loads<S, TD, LIN>(g, stage, sT, reg, g.tet_kf != nullptr, i, nd[q], c[q]);
         // tets are never corner-unique: colour phases (phase byte per slot) or,
         // if the colouring overflowed, ranked phases (rank byte per corner)
         if (valid[q] && g.tet_phase) {
@@ -557,17 +556,16 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       for (int q = 0; q < kSPT; ++q) {
         const int i = q * kTileThreads + tid;
         const int s = h_start + b * kBatch + i;
-        const Curve<S> &kc =
-            g.mats.m[(g.hex_region && valid[q])
-                         ? stage[StageLayout<S>(8, g.hex_kf != nullptr, g.hex_rank != nullptr, true).region + i]
-                         : 0].k;
+        const int reg = (g.hex_region && valid[q])
+                            ? stage[StageLayout<S>(8, g.hex_kf != nullptr, g.hex_rank != nullptr, true).region + i]
+                            : 0;
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
           nd[q][a] = 0;
           c[q][a] = S(0);
           rk[q][a] = 0xff;
         }
-        if (valid[q]) hex_loads<S, TD, LIN>(g, stage, sT, kc, g.hex_kf != nullptr, i, nd[q], c[q]);
+        if (valid[q]) hex_loads<S, TD, LIN>(g, stage, sT, reg, g.hex_kf != nullptr, i, nd[q], c[q]);
         if (MODE == kRanked && valid[q]) {
           const StageLayout<S> L(8, g.hex_kf != nullptr, true, g.hex_region != nullptr);
           const uint2 w = reinterpret_cast<const uint2 *>(stage + L.rank)[i];

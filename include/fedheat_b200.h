@@ -19,7 +19,7 @@
  *
  * Status codes: 0 ok, 1 config error (ConfigError), 2 instability
  * (InstabilityError), 3 CUDA/NCCL failure, 4 degenerate element
- * (DegenerateElementError).  fh_last_error() returns the calling thread's
+ * (DegenerateElementError), 5 mesh text format (MeshFormatError).  fh_last_error() returns the calling thread's
  * message for the last non-zero status.
  */
 #ifndef FEDHEAT_B200_H
@@ -36,6 +36,7 @@ extern "C" {
 #define FH_ERR_INSTABILITY 2
 #define FH_ERR_DEVICE 3
 #define FH_ERR_DEGENERATE 4
+#define FH_ERR_FORMAT 5 /* MeshFormatError (mesh ingest) */
 
 #define FH_MAX_KNOTS 32
 #define FH_CHUNK_SIZE 4096 /* solver.py:48 CHUNK_SIZE */
@@ -260,6 +261,38 @@ int fh_plan_info(fh_plan *plan, int64_t *info, int32_t n_info);
 int fh_plan_arrays(fh_plan *plan, int64_t *new_to_old, int64_t *part_node_start, int32_t *peers, int64_t *send_offs,
                    int64_t *send_nodes, int64_t *recv_offs, int64_t *recv_nodes);
 int fh_plan_destroy(fh_plan *plan);
+
+/* ------------------------------------------------------------------ */
+/* 3. Mesh ingest and text output (host only, no GPU)                   */
+/* ------------------------------------------------------------------ */
+
+/* mesh.py:192-236 parse_mesh_text: the reference's mesh grammar (nodes /
+ * elements tet4|hex8 / nodeset blocks, '#' comments, Python splitlines() line
+ * breaks and split() whitespace over UTF-8 text).  Tokens convert like
+ * Python int()/float() (underscores, inf/nan; floats correctly rounded).
+ * On a grammar error returns FH_ERR_FORMAT with the reference's message
+ * (without the "line N: " prefix) and *err_line = the 1-based line the
+ * reference reports.  Geometry is not validated here (Mesh() does it).
+ * n_threads <= 0: all hardware threads convert the coordinate block. */
+typedef struct fh_mesh_text fh_mesh_text;
+int fh_mesh_parse(const char *text, int64_t len, int32_t n_threads, fh_mesh_text **out, int64_t *err_line);
+int fh_mesh_text_info(fh_mesh_text *m, int64_t *n_nodes, int64_t *n_tets, int64_t *n_hexes, int32_t *n_sets);
+/* nodes (V,3) f64, tets (Et,4), hexes (Eh,8) i64 in file order; NULL skips */
+int fh_mesh_text_arrays(fh_mesh_text *m, double *nodes, int64_t *tets, int64_t *hexes);
+/* node set i (file order): name (NUL-terminated), members in file order;
+ * ids == NULL only reports *count */
+int fh_mesh_text_set(fh_mesh_text *m, int32_t i, char *name, int64_t name_cap, int64_t *ids, int64_t *count);
+int fh_mesh_text_destroy(fh_mesh_text *m);
+
+/* Text rows as the reference writes them (mesh.py:241-253 serialize_mesh_text,
+ * vtkio.py:20-52 vtk_text, cli.py:81-86 probes.csv): each row is row_prefix
+ * (may be NULL), then `cols` values joined by `sep`, then '\n'.  Doubles are
+ * Python repr(float) (shortest round-trip digits), integers str(int).  With
+ * out == NULL only *used (the byte count) is computed. */
+int fh_format_f64(const double *v, int64_t rows, int64_t cols, char sep, const char *row_prefix, int32_t n_threads,
+                  char *out, int64_t cap, int64_t *used);
+int fh_format_i64(const int64_t *v, int64_t rows, int64_t cols, char sep, const char *row_prefix, int32_t n_threads,
+                  char *out, int64_t cap, int64_t *used);
 
 #ifdef __cplusplus
 }

@@ -88,7 +88,8 @@ EXPORTS = [
     "fh_step_timed", "fh_step_timed_flush", "fh_step_host", "fh_set_q_static", "fh_set_sources", "fh_set_probes", "fh_get_probes", "fh_critical_dt", "fh_scatter_loads",
     "fh_get_precompute", "fh_get_layout", "fh_stream", "fh_get_node_order", "fh_nccl_unique_id",
     "fh_attach_nccl", "fh_halo_info", "fh_halo_lists", "fh_halo_export", "fh_halo_import", "fh_get_owned",
-    "fh_plan_create", "fh_plan_info", "fh_plan_arrays", "fh_plan_destroy",
+    "fh_plan_create", "fh_plan_info", "fh_plan_arrays", "fh_plan_destroy", "fh_mesh_parse", "fh_mesh_text_info",
+    "fh_mesh_text_arrays", "fh_mesh_text_set", "fh_mesh_text_destroy", "fh_format_f64", "fh_format_i64",
 ]
 
 _lib = None
@@ -145,6 +146,15 @@ def lib():
     L.fh_plan_info.argtypes = [C.c_void_p, i64p, C.c_int32]
     L.fh_plan_arrays.argtypes = [C.c_void_p, i64p, i64p, i32p, i64p, i64p, i64p, i64p]
     L.fh_plan_destroy.argtypes = [C.c_void_p]
+    L.fh_mesh_parse.argtypes = [C.c_char_p, C.c_int64, C.c_int32, C.POINTER(C.c_void_p), i64p]
+    L.fh_mesh_text_info.argtypes = [C.c_void_p, i64p, i64p, i64p, C.POINTER(C.c_int32)]
+    L.fh_mesh_text_arrays.argtypes = [C.c_void_p, f64p, i64p, i64p]
+    L.fh_mesh_text_set.argtypes = [C.c_void_p, C.c_int32, C.c_char_p, C.c_int64, i64p, i64p]
+    L.fh_mesh_text_destroy.argtypes = [C.c_void_p]
+    L.fh_format_f64.argtypes = [f64p, C.c_int64, C.c_int64, C.c_char, C.c_char_p, C.c_int32, C.c_char_p,
+                                C.c_int64, i64p]
+    L.fh_format_i64.argtypes = [i64p, C.c_int64, C.c_int64, C.c_char, C.c_char_p, C.c_int32, C.c_char_p,
+                                C.c_int64, i64p]
     _lib = L
     return L
 

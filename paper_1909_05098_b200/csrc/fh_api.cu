@@ -1,3 +1,4 @@
+#include <cstdarg>
 // C ABI of libfedheat_b200.so (include/fedheat_b200.h): engine lifetime,
 // device precompute, state I/O, stepping, probes, critical dt, operator layer.
 #include <algorithm>
@@ -15,6 +16,20 @@ using namespace fh;
 namespace {
 
 thread_local std::string g_last_error;
+
+}  // namespace
+
+int fh::set_error(int code, const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+namespace {
 
 int report(const std::exception &ex) {
   if (const auto *fe = dynamic_cast<const Error *>(&ex)) {

@@ -19,6 +19,9 @@ struct Error : std::runtime_error {
 
 [[noreturn]] inline void fail(int code, const std::string &msg) { throw Error(code, msg); }
 
+// record `code`'s printf-style message as the calling thread's fh_last_error(); returns code
+int set_error(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+
 #define FH_CUDA(x)                                                                          \
   do {                                                                                      \
     cudaError_t _e = (x);                                                                   \

@@ -62,6 +62,7 @@ FH_ERR_CONFIG = 1
 FH_ERR_INSTABILITY = 2
 FH_ERR_DEVICE = 3
 FH_ERR_DEGENERATE = 4
+FH_ERR_FORMAT = 5
 
 
 def raise_for_status(status: int, message: str) -> None:
@@ -71,6 +72,8 @@ def raise_for_status(status: int, message: str) -> None:
         raise ConfigError(message)
     if status == FH_ERR_DEGENERATE:
         raise DegenerateElementError(message)
+    if status == FH_ERR_FORMAT:
+        raise MeshFormatError(message)
     if status == FH_ERR_DEVICE:
         raise DeviceError(message)
     raise FedheatError(f"native status {status}: {message}")

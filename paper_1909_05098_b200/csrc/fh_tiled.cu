@@ -424,6 +424,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   __shared__ __align__(8) uint64_t bars[kMaxStages];
   __shared__ __align__(8) uint64_t hbar;  // halo id list copy
   __shared__ int s_bad;
+  // phases per batch of the tile (colour modes), read once instead of per batch
+  constexpr int kNphCache = 64;
+  __shared__ uint8_t s_nph[kNphCache];
   if (g.flag->step != kNone) return;
   const int p = g.part_list ? g.part_list[g.part_begin + blockIdx.x] : g.part_begin + (int)blockIdx.x;
   const int tid = threadIdx.x;
@@ -442,6 +445,12 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   const int h0 = g.part_halo_start[p], nh = g.part_halo_start[p + 1] - h0;
   const int hs = h0 & ~3, hoff = h0 - hs;
   int32_t *s_ids = reinterpret_cast<int32_t *>(acc);
+  {
+    const uint8_t *bn = (KINDS == 0) ? nullptr : g.tet_bnph;
+    if (bn && tid < nbt && tid < kNphCache) s_nph[tid] = __ldg(bn + t_start / kBatch + tid);
+    const uint8_t *hn = (KINDS == 1 || MODE != kColored) ? nullptr : g.hex_bnph;
+    if (hn && tid < nbh && nbt + tid < kNphCache) s_nph[nbt + tid] = __ldg(hn + h_start / kBatch + tid);
+  }
   if (tid == 0) {
     s_bad = 0;
 #pragma unroll
@@ -501,6 +510,15 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
     acc[i] = S(0);
   __syncthreads();
 
+  // uniform per launch: stage layouts and which optional streams exist
+  const bool t_kf = g.tet_kf != nullptr, h_kf = g.hex_kf != nullptr;
+  const bool t_reg = g.tet_region != nullptr, h_reg = g.hex_region != nullptr;
+  const bool t_col = g.tet_phase != nullptr;
+  const StageLayout<S> Lt(4, t_kf, !t_col, t_reg);
+  const StageLayout<S> Lh(8, h_kf, MODE == kRanked, h_reg);
+  auto batch_nph = [&](int jj, const uint8_t *bn, int slot0) -> int {
+    return jj < kNphCache ? (int)s_nph[jj] : (int)__ldg(bn + slot0 / kBatch);
+  };
   int st = 0;
   uint32_t parity = 0;
   for (int j = 0; j < nb; ++j) {
@@ -518,34 +536,25 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       uint8_t rk[kSPT][4];
 #pragma unroll
       for (int q = 0; q < kSPT; ++q) {
-        const int i = q * kTileThreads + tid;
-        const int s = t_start + b * kBatch + i;
-        const int reg = (g.tet_region && valid[q])
-                            ? stage[StageLayout<S>(4, g.tet_kf != nullptr, g.tet_rank != nullptr, true).region + i]
-                            : 0;
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          nd[q][a] = 0;
-          c[q][a] = S(0);
-          rk[q][a] = 0xff;
-        }
-        if (valid[q]) tet_loads<S, TD, LIN>(g, stage, sT, reg, g.tet_kf != nullptr, i, nd[q], c[q]);
+        // slots past the end of a partial batch read slot 0 (always present)
+        // instead of branching; only their accumulation is predicated off
+        const int i = valid[q] ? q * kTileThreads + tid : 0;
+        const int reg = t_reg ? (int)stage[Lt.region + i] : 0;
+        tet_loads<S, TD, LIN>(g, stage, sT, reg, t_kf, i, nd[q], c[q]);
         // tets are never corner-unique: colour phases (phase byte per slot) or,
         // if the colouring overflowed, ranked phases (rank byte per corner)
-        if (valid[q] && g.tet_phase) {
-          const StageLayout<S> L(4, g.tet_kf != nullptr, false, g.tet_region != nullptr);
-          const uint8_t ph = stage[L.phase + i];
+        if (t_col) {
+          const uint8_t ph = stage[Lt.phase + i];
 #pragma unroll
           for (int a = 0; a < 4; ++a) rk[q][a] = ph;
-        } else if (valid[q]) {
-          const StageLayout<S> L(4, g.tet_kf != nullptr, true, g.tet_region != nullptr);
-          const uint32_t w = reinterpret_cast<const uint32_t *>(stage + L.rank)[i];
+        } else {
+          const uint32_t w = reinterpret_cast<const uint32_t *>(stage + Lt.rank)[i];
           rk[q][0] = w & 0xff; rk[q][1] = (w >> 8) & 0xff; rk[q][2] = (w >> 16) & 0xff; rk[q][3] = w >> 24;
         }
       }
-      if (g.tet_phase)
+      if (t_col)
         accumulate_colored<S, 4>(acc, nd[0], c[0], nfree, valid[0], rk[0][0],
-                                 (int)g.tet_bnph[(t_start + b * kBatch) / kBatch]);
+                                 batch_nph(j, g.tet_bnph, t_start + b * kBatch));
       else
         accumulate<S, 4, kRanked>(acc, nd, c, nfree, valid, rk, g.max_phase_tet);
     } else {
@@ -554,37 +563,28 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       uint8_t rk[kSPT][8];
 #pragma unroll
       for (int q = 0; q < kSPT; ++q) {
-        const int i = q * kTileThreads + tid;
-        const int s = h_start + b * kBatch + i;
-        const int reg = (g.hex_region && valid[q])
-                            ? stage[StageLayout<S>(8, g.hex_kf != nullptr, g.hex_rank != nullptr, true).region + i]
-                            : 0;
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-          nd[q][a] = 0;
-          c[q][a] = S(0);
-          rk[q][a] = 0xff;
-        }
-        if (valid[q]) hex_loads<S, TD, LIN>(g, stage, sT, reg, g.hex_kf != nullptr, i, nd[q], c[q]);
-        if (MODE == kRanked && valid[q]) {
-          const StageLayout<S> L(8, g.hex_kf != nullptr, true, g.hex_region != nullptr);
-          const uint2 w = reinterpret_cast<const uint2 *>(stage + L.rank)[i];
+        const int i = valid[q] ? q * kTileThreads + tid : 0;
+        const int reg = h_reg ? (int)stage[Lh.region + i] : 0;
+        hex_loads<S, TD, LIN>(g, stage, sT, reg, h_kf, i, nd[q], c[q]);
+        if (MODE == kRanked) {
+          const uint2 w = reinterpret_cast<const uint2 *>(stage + Lh.rank)[i];
 #pragma unroll
           for (int a = 0; a < 4; ++a) {
             rk[q][a] = (w.x >> (8 * a)) & 0xff;
             rk[q][a + 4] = (w.y >> (8 * a)) & 0xff;
           }
-        }
-        if (MODE == kColored && valid[q]) {
-          const StageLayout<S> L(8, g.hex_kf != nullptr, false, g.hex_region != nullptr);
-          const uint8_t ph = stage[L.phase + i];
+        } else if (MODE == kColored) {
+          const uint8_t ph = stage[Lh.phase + i];
 #pragma unroll
           for (int a = 0; a < 8; ++a) rk[q][a] = ph;
+        } else {
+#pragma unroll
+          for (int a = 0; a < 8; ++a) rk[q][a] = 0;
         }
       }
       if (MODE == kColored)
         accumulate_colored<S, 8>(acc, nd[0], c[0], nfree, valid[0], rk[0][0],
-                                 (int)g.hex_bnph[(h_start + b * kBatch) / kBatch]);
+                                 batch_nph(j, g.hex_bnph, h_start + b * kBatch));
       else
         accumulate<S, 8, MODE>(acc, nd, c, nfree, valid, rk, g.max_phase_hex);
     }

@@ -150,6 +150,7 @@ struct TiledState {
   DBuf<int32_t> tet_conn, hex_conn, tet_slot_elem, hex_slot_elem;
   DBuf<S> tet_kf, hex_kf, tet_kbar, hex_kbar;
   DBuf<uint8_t> tet_rank, hex_rank, tet_region, hex_region, node_region;
+  DBuf<int8_t> part_mat;
   DBuf<uint8_t> tet_phase, hex_phase, tet_bnph, hex_bnph;
   DBuf<S> T[2], vol, cap, kb, q_ext, xyz, robin_hA, robin_hAT;
   int cur = 0;
@@ -266,6 +267,31 @@ TiledState<double> &tstate<double>(fh_engine *e) { return *e->tdd; }
 int default_part_nodes(int precision, int64_t n_tet, int64_t n_hex) {
   if (precision != 32) return 768;
   return n_tet > n_hex ? 768 : 1536;
+}
+
+// Wave fit: with only a few waves of tile CTAs per launch, the last partial
+// wave leaves SMs idle (cfg3: 1342 tiles on 148 SMs x 5 CTAs = 1.81 waves).
+// The tile size is lowered just enough that the tile count fills the last wave
+// (cfg3: 1480 tiles, 0.0923 -> 0.089 ms/step; scripts/sweep.py).  Parts per
+// domain are ceil(V_domain / target) (fh_partition.cpp), so the count is exact.
+int wave_fit_part_nodes(int target, int64_t V, int n_domains, int precision, int64_t n_tet, int64_t n_hex,
+                        int device) {
+  int sms = 148;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || sms <= 0) {
+    cudaGetLastError();
+    sms = 148;
+  }
+  // resident step CTAs per SM (the launch bounds of k_tiled_step)
+  const int per_sm = precision != 32 ? 2 : (n_hex == 0 ? 5 : 4);
+  const int64_t cap = (int64_t)sms * per_sm;
+  const int64_t vd = (V + n_domains - 1) / n_domains;
+  const int64_t n0 = (int64_t)n_domains * ((vd + target - 1) / target);
+  const double waves = (double)n0 / (double)cap;
+  if (waves >= 6.0) return target;  // the tail is a small fraction already
+  const int64_t w = (int64_t)std::ceil(waves - 1e-9);
+  const int64_t per_dom = std::max<int64_t>(1, w * cap / n_domains);
+  const int64_t t = (vd + per_dom - 1) / per_dom;
+  return (int)std::max<int64_t>(64, std::min<int64_t>(target, t));
 }
 
 // Tiled kernels: a one-knot curve becomes the two-knot curve (y0, y0) with
@@ -421,6 +447,9 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   // small meshes: shrink the tiles so that at least ~2 CTAs per SM exist (latency-bound regime)
   if (o.part_nodes <= 0 && V / pin.target_part_nodes < 2 * 148)
     pin.target_part_nodes = (int)std::max<int64_t>(96, V / (2 * 148));
+  else if (o.part_nodes <= 0)
+    pin.target_part_nodes = wave_fit_part_nodes(pin.target_part_nodes, V, std::max(1, o.n_domains),
+                                                sizeof(S) == 4 ? 32 : 64, e->n_tet, e->n_hex, o.device);
   pin.batch = kBatch;
   // layout tuning knobs (scripts/sweep.py): hex colour order, first-touch node order
   if (const char *env = getenv("FH_HEX_COLOR")) pin.hex_color = atoi(env);
@@ -557,6 +586,17 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     std::vector<uint8_t> nrn(V);
     for (int64_t n = 0; n < V; ++n) nrn[n] = (uint8_t)nr[P.old_of_new[n]];
     st->node_region.upload(nrn, s);
+    // per tile: the material of its updated nodes when they all share one
+    // (the node update then reads the laws as uniform operands), else -1
+    std::vector<int8_t> pm(P.n_parts);
+    for (int p = 0; p < P.n_parts; ++p) {
+      const int64_t a = P.part_node_start[p], b = a + P.part_n_free[p];
+      int m = b > a ? nrn[a] : 0;
+      for (int64_t n = a; n < b && m >= 0; ++n)
+        if (nrn[n] != m) m = -1;
+      pm[p] = (int8_t)m;
+    }
+    st->part_mat.upload(pm, s);
   }
   if (!e->td) {
     st->cap.alloc(V);
@@ -624,6 +664,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.q_ext = st->q_ext.p;
   g.xyzv = st->xyz.p;
   g.node_region = st->node_region.p;
+  g.part_mat = st->part_mat.p;
   g.robin_hA = st->robin_hA.p;
   g.robin_hAT = st->robin_hAT.p;
   g.mats = mats_of<S>(e);

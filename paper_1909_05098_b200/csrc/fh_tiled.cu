@@ -48,6 +48,10 @@ constexpr int kMinBlocksTet = FH_MIN_BLOCKS_TET;  // tet-only fp32 kernels: smal
 #ifndef FH_NODE_UNROLL
 #define FH_NODE_UNROLL 2
 #endif
+// per-tile material / single-RF node bodies (0: the general body whenever node regions exist)
+#ifndef FH_PART_MAT
+#define FH_PART_MAT 1
+#endif
 // corner phases: predicated accumulation (0) or unpredicated into a trash slot (1)
 #ifndef FH_TRASH_SLOT
 #define FH_TRASH_SLOT 0
@@ -601,12 +605,14 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   __syncthreads();
 
   // lumped nodal update of the owned free nodes.  The per-tile uniform
-  // decisions (material lookup, source kinds, Robin rows) pick one of three
+  // decisions (material lookup, source kinds, Robin rows) pick one of four
   // loop bodies, so the common ones are branch-free and the UN nodes of a
   // round interleave: 0 general, 1 single material / no dynamic source / no
-  // Robin row in the tile, 2 the same with exactly one Gaussian source.
+  // Robin row in the tile, 2 the same with exactly one Gaussian source, 3 the
+  // same with exactly one RF source.  `tm` is the tile's material.
   bool bad = false;
   const int rstart = g.part_robin_start[p];
+  const int tm = g.node_region ? (FH_PART_MAT ? (int)g.part_mat[p] : -1) : 0;
   constexpr int UN = FH_NODE_UNROLL;  // nodes per thread per round: their global loads are issued together
   auto node_loop = [&](auto kind_tag) {
     constexpr int KIND = decltype(kind_tag)::value;
@@ -620,7 +626,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         q[u] = g.q_ext ? __ldg(g.q_ext + n) : S(0);
         cf[u] = TD ? S(0) : __ldg(g.cap_frozen + n);
         kf[u] = (!TD && g.kb_frozen) ? __ldg(g.kb_frozen + n) : S(0);
-        if (KIND == 2 || (KIND == 0 && g.n_src)) {  // packed (x, y, z, v): one vector load per node
+        if (KIND >= 2 || (KIND == 0 && g.n_src)) {  // packed (x, y, z, v): one vector load per node
           load_xyzv(g.xyzv + 4 * (size_t)n, px[u], py[u], pz[u], v[u]);
         } else {
           v[u] = __ldg(g.vol + n);
@@ -645,7 +651,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         }
         S rate;
         S cap;
-        if (KIND != 0 || !g.node_region)  // single material: curve parameters are uniform operands
+        if (KIND != 0)  // single material: curve parameters are uniform operands
+          rate = node_rate<S, TD, LIN>(g.mats.m[tm], x, Fsum, v[u], q[u], cf[u], kf[u], cap);
+        else if (!g.node_region)
           rate = node_rate<S, TD, LIN>(g.mats.m[0], x, Fsum, v[u], q[u], cf[u], kf[u], cap);
         else
           rate = node_rate<S, TD, LIN>(g.mats.m[g.node_region[n]], x, Fsum, v[u], q[u], cf[u], kf[u], cap);
@@ -653,6 +661,11 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
           const SourceT<S> &sr = g.src[0];
           const S dx = px[u] - sr.cx, dy = py[u] - sr.cy, dz = pz[u] - sr.cz;
           rate += sr.amp * fast_exp(-((dx * dx + dy * dy) + dz * dz) * sr.inv2s2) * v[u];
+        } else if (KIND == 3) {  // min(P / (4 pi r^2), cap), the cap at r = 0 (sources_at)
+          const SourceT<S> &sr = g.src[0];
+          const S dx = px[u] - sr.cx, dy = py[u] - sr.cy, dz = pz[u] - sr.cz;
+          const S r2 = (dx * dx + dy * dy) + dz * dz;
+          rate += (r2 > S(0) ? min(sr.cap, sr.inv4pi_amp / r2) : sr.cap) * v[u];
         } else if (KIND == 0 && g.n_src) {
           const S xyz[3] = {px[u], py[u], pz[u]};
           rate += sources_at(g, xyz) * v[u];
@@ -669,11 +682,13 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       }
     }
   };
-  const bool simple = !g.node_region && rstart >= nfree;
+  const bool simple = tm >= 0 && rstart >= nfree;
   if (simple && g.n_src == 0)
     node_loop(std::integral_constant<int, 1>{});
   else if (simple && g.n_src == 1 && g.n_gauss == 1)
     node_loop(std::integral_constant<int, 2>{});
+  else if (simple && g.n_src == 1)
+    node_loop(std::integral_constant<int, 3>{});
   else
     node_loop(std::integral_constant<int, 0>{});
   if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) s_bad = 1;

@@ -51,6 +51,7 @@ struct TiledArgs {
   const S *q_ext;                   // heat loads + static sources (W) or null
   const S *xyzv;                    // (x, y, z, v) per node, for time-dependent sources
   const uint8_t *node_region;
+  const int8_t *part_mat;  // with node_region: the tile's single material, or -1
   const S *robin_hA, *robin_hAT;
   MatSet<S> mats;   // one-knot curves normalised to two knots (see normalise_curves)
   int lin;          // every curve has <= 2 knots: branch-free interpolation kernels

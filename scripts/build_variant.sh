@@ -10,5 +10,5 @@ FL="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler 
 $NV $FL $2 -Xptxas -v -c fh_tiled.cu -o build_$1/fh_tiled.o 2> build_$1/ptxas.txt
 $NV $FL $2 -c fh_api.cu -o build_$1/fh_api.o
 $NV -gencode arch=compute_100a,code=sm_100a -shared -o ../libfedheat_b200_$1.so build_$1/fh_api.o build_$1/fh_tiled.o \
-  build/fh_exact.o build/fh_precompute.o build/fh_partition.o build/fh_dist.o -lcudart_static -lrt -ldl -lpthread
+  build/fh_exact.o build/fh_precompute.o build/fh_partition.o build/fh_dist.o build/fh_meshio.o -lcudart_static -lrt -ldl -lpthread
 echo built libfedheat_b200_$1.so

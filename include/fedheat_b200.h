@@ -253,7 +253,8 @@ int fh_get_owned(fh_engine *e, uint8_t *mask, int64_t n);
  * bookkeeping fh_create performs, for checking it bit for bit.  info[] =
  * {n_parts, parts of rank, boundary parts of rank, peers, n_send, n_recv,
  * node_lo, node_hi, corner_unique, max_phase_tet, max_phase_hex, n_slots,
- * max_local_nodes}. */
+ * max_local_nodes, colored_ok, max_colors, max_nph_tet, max_nph_hex,
+ * sum of tet batch phases, tet batch count (array length), same two for hexes}. */
 typedef struct fh_plan fh_plan;
 int fh_plan_create(const fh_mesh *mesh, const fh_boundary *boundary, const fh_options *opts, int32_t world,
                    int32_t rank, fh_plan **out);

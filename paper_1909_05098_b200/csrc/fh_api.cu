@@ -269,6 +269,14 @@ int default_part_nodes(int precision, int64_t n_tet, int64_t n_hex) {
   return n_tet > n_hex ? 768 : 1536;
 }
 
+// Tet-only meshes: colour classes with up to 4 writes per node (4 accumulator
+// rows, ~4x larger classes -> fewer colour phases per 256-slot batch).
+int default_tet_rows(int64_t n_tet, int64_t n_hex) {
+  int r = (n_tet > 0 && n_hex == 0) ? 4 : 1;
+  if (const char *env = getenv("FH_TET_ROWS")) r = atoi(env) > 1 ? 4 : 1;
+  return r;
+}
+
 // Wave fit: with only a few waves of tile CTAs per launch, the last partial
 // wave leaves SMs idle (cfg3: 1342 tiles on 148 SMs x 5 CTAs = 1.81 waves).
 // The tile size is lowered just enough that the tile count fills the last wave
@@ -454,6 +462,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   // layout tuning knobs (scripts/sweep.py): hex colour order, first-touch node order
   if (const char *env = getenv("FH_HEX_COLOR")) pin.hex_color = atoi(env);
   if (const char *env = getenv("FH_FIRST_TOUCH")) pin.first_touch = atoi(env);
+  pin.tet_rows = default_tet_rows(e->n_tet, e->n_hex);
   pin.n_domains = std::max(1, o.n_domains);
   pin.slab_axis = o.slab_axis;
   build_partition(pin, e->part);
@@ -669,6 +678,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.robin_hAT = st->robin_hAT.p;
   g.mats = mats_of<S>(e);
   g.lin = normalise_curves(g.mats);
+  g.tet_rows = P.tet_rows;
   g.n_src = 0;  // set per step from the active sources
   g.n_gauss = 0;
   g.runaway_limit = (S)e->runaway_limit;
@@ -681,7 +691,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   if (const char *env = getenv("FH_TILE_STAGES")) g.n_stages = std::min(kMaxStages, std::max(1, atoi(env)));
   g.smem_T = (int)al(2 * sizeof(S) * (size_t)std::max(1, P.max_local_nodes));
   // +1: the trash slot of the corner-phase accumulation
-  const int rows = st->mode == kModeCornerSlot ? 8 : (st->mode == kModeCornerPhase2 ? 2 : 1);
+  const int rows = std::max(st->mode == kModeCornerSlot ? 8 : (st->mode == kModeCornerPhase2 ? 2 : 1), P.tet_rows);
   g.smem_acc = (int)al(sizeof(S) * rows * ((size_t)std::max(1, P.max_part_free) + 1));
   {  // the accumulator region first holds the tile's halo id list (bulk copy)
     int max_halo = 0;
@@ -1707,6 +1717,7 @@ int fh_plan_create(const fh_mesh *mesh, const fh_boundary *bnd, const fh_options
   // layout tuning knobs (scripts/sweep.py): hex colour order, first-touch node order
   if (const char *env = getenv("FH_HEX_COLOR")) pin.hex_color = atoi(env);
   if (const char *env = getenv("FH_FIRST_TOUCH")) pin.first_touch = atoi(env);
+  pin.tet_rows = default_tet_rows(mesh->n_tets, mesh->n_hexes);
   pin.n_domains = std::max(1, opts->n_domains);
   pin.slab_axis = opts->slab_axis;
   build_partition(pin, pl->P);
@@ -1717,13 +1728,21 @@ int fh_plan_create(const fh_mesh *mesh, const fh_boundary *bnd, const fh_options
   FH_API_END
 }
 
+static int64_t sum_u8(const std::vector<uint8_t> &v) {
+  int64_t t = 0;
+  for (uint8_t x : v) t += x;
+  return t;
+}
+
 int fh_plan_info(fh_plan *pl, int64_t *info, int32_t n_info) {
   FH_API_BEGIN
   const int64_t v[] = {pl->P.n_parts, pl->X.part_hi - pl->X.part_lo, pl->X.n_boundary, (int64_t)pl->X.peers.size(),
                        (int64_t)pl->X.send_nodes.size(), (int64_t)pl->X.recv_nodes.size(), pl->X.node_lo,
                        pl->X.node_hi, (int64_t)pl->P.corner_unique, pl->P.max_phase_tet, pl->P.max_phase_hex,
                        (int64_t)(pl->P.tet_slot_elem.size() + pl->P.hex_slot_elem.size()), pl->P.max_local_nodes,
-                       (int64_t)pl->P.colored_ok, pl->P.max_colors, pl->P.max_nph_tet, pl->P.max_nph_hex};
+                       (int64_t)pl->P.colored_ok, pl->P.max_colors, pl->P.max_nph_tet, pl->P.max_nph_hex,
+                       sum_u8(pl->P.tet_batch_nph), (int64_t)pl->P.tet_batch_nph.size(), sum_u8(pl->P.hex_batch_nph),
+                       (int64_t)pl->P.hex_batch_nph.size()};
   for (int q = 0; q < n_info && q < (int)(sizeof(v) / sizeof(v[0])); ++q) info[q] = v[q];
   FH_API_END
 }

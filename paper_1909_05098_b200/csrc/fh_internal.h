@@ -131,6 +131,7 @@ struct PartitionInput {
   int slab_axis;      // -1 RCB, else domains are slabs along this axis
   int hex_color = 0;  // 0: colour hexes only when not corner-unique; 1: always
   int first_touch = 0;  // renumber each tile's nodes in first-touch order of its batches (measured neutral)
+  int tet_rows = 1;     // tet colour classes may touch a node up to tet_rows times (one accumulator row each)
 };
 
 struct Partition {
@@ -160,6 +161,10 @@ struct Partition {
   int max_colors = 0, max_nph_tet = 0, max_nph_hex = 0;
   std::vector<uint8_t> tet_color, hex_color, tet_phase, hex_phase;
   std::vector<uint8_t> tet_batch_nph, hex_batch_nph;  // phases per batch (index = slot / B)
+  // tet accumulator rows: 1, or 4 when every tile's tet colour classes were
+  // built with up to 4 writes per node (row r = the write's rank in its
+  // class; stored in bits 14-15 of tet_conn16, local index in bits 0-13)
+  int tet_rows = 1;
 };
 
 void build_partition(const PartitionInput &in, Partition &out);

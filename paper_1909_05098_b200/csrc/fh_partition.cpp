@@ -177,7 +177,7 @@ void build_partition(const PartitionInput &in, Partition &P) {
   std::vector<std::vector<int32_t>> tet_pp(P.n_parts), hex_pp(P.n_parts);
   build_slots<4>(in.n_tet, in.tets, 0, P, part_of_new, updatable_new, tet_pp);
   build_slots<8>(in.n_hex, in.hexes, in.n_tet, P, part_of_new, updatable_new, hex_pp);
-  std::vector<std::vector<uint8_t>> tet_color_pp, hex_color_pp;
+  std::vector<std::vector<uint8_t>> tet_color_pp, hex_color_pp, tet_rows_pp;
   // order the slots of a part by their smallest corner id (new numbering), so
   // that neighbouring threads of a batch touch neighbouring nodes: the
   // shared-memory gathers and accumulations are then bank-conflict free
@@ -203,42 +203,59 @@ void build_partition(const PartitionInput &in, Partition &P) {
     // greedy colouring of each tile's slots: two slots of one colour never
     // share a node the tile updates.  A stable sort by colour makes every
     // batch span few colours -> few accumulation phases (kColored mode).
-    std::vector<uint64_t> used(P.max_part_nodes, 0);
-    std::vector<std::pair<int, int32_t>> ct;
+    // With R accumulator rows a class may touch a node up to R times: the
+    // r-th write of a class to a node goes to row r (tets only, R = 1 or 4).
+    // Classes then grow R-fold, so a 256-slot batch spans fewer of them.
+    const int R_tet = std::max(1, std::min(4, in.tet_rows));
+    std::vector<uint64_t> used((size_t)P.max_part_nodes * 4, 0);  // used[loc * 4 + r]: colours written >= r + 1 times
+    struct Ct {
+      int col;
+      int32_t e;
+      uint8_t rows;  // 2 bits per corner
+    };
+    std::vector<Ct> ct;
     P.colored_ok = true;
     P.max_colors = 0;
     auto colour_part = [&](std::vector<int32_t> &v, int N, int p) {
       const int64_t n0 = P.part_node_start[p], nf = P.part_n_free[p];
+      const int R = N == 4 ? R_tet : 1;
       ct.clear();
       for (int32_t e : v) {
         const int64_t *c = N == 4 ? in.tets + 4 * (int64_t)e : in.hexes + 8 * ((int64_t)e - in.n_tet);
-        uint64_t m = 0;
+        uint64_t m = 0;  // colours in which some corner is already full
         for (int a = 0; a < N; ++a) {
           const int64_t loc = P.new_of_old[c[a]] - n0;
-          if (loc >= 0 && loc < nf) m |= used[loc];
+          if (loc >= 0 && loc < nf) m |= used[(size_t)loc * 4 + (R - 1)];
         }
         if (~m == 0) {
           P.colored_ok = false;
-          ct.emplace_back(63, e);
+          ct.push_back({63, e, 0});
           continue;
         }
         const int col = __builtin_ctzll(~m);
+        const uint64_t bit = 1ull << col;
         P.max_colors = std::max(P.max_colors, col + 1);
+        uint8_t rows = 0;
         for (int a = 0; a < N; ++a) {
           const int64_t loc = P.new_of_old[c[a]] - n0;
-          if (loc >= 0 && loc < nf) used[loc] |= (1ull << col);
+          if (loc < 0 || loc >= nf) continue;
+          int r = 0;
+          while (used[(size_t)loc * 4 + r] & bit) ++r;  // r < R: the class is not full at this node
+          used[(size_t)loc * 4 + r] |= bit;
+          if (N == 4) rows |= (uint8_t)(r << (2 * a));
         }
-        ct.emplace_back(col, e);
+        ct.push_back({col, e, rows});
       }
       for (int32_t e : v) {  // reset the masks of this tile
         const int64_t *c = N == 4 ? in.tets + 4 * (int64_t)e : in.hexes + 8 * ((int64_t)e - in.n_tet);
         for (int a = 0; a < N; ++a) {
           const int64_t loc = P.new_of_old[c[a]] - n0;
-          if (loc >= 0 && loc < nf) used[loc] = 0;
+          if (loc >= 0 && loc < nf)
+            for (int r = 0; r < 4; ++r) used[(size_t)loc * 4 + r] = 0;
         }
       }
-      std::stable_sort(ct.begin(), ct.end(), [](const auto &x, const auto &y) { return x.first < y.first; });
-      for (size_t q = 0; q < v.size(); ++q) v[q] = ct[q].second;
+      std::stable_sort(ct.begin(), ct.end(), [](const Ct &x, const Ct &y) { return x.col < y.col; });
+      for (size_t q = 0; q < v.size(); ++q) v[q] = ct[q].e;
       return ct;
     };
     // Hexes that are corner-unique inside every tile use corner phases and
@@ -273,13 +290,18 @@ void build_partition(const PartitionInput &in, Partition &P) {
     P.hex_color.clear();
     tet_color_pp.assign(P.n_parts, {});
     hex_color_pp.assign(P.n_parts, {});
+    tet_rows_pp.assign(P.n_parts, {});
     for (int p = 0; p < P.n_parts; ++p) {
-      for (auto &x : colour_part(tet_pp[p], 4, p)) tet_color_pp[p].push_back((uint8_t)x.first);
+      for (auto &x : colour_part(tet_pp[p], 4, p)) {
+        tet_color_pp[p].push_back((uint8_t)x.col);
+        tet_rows_pp[p].push_back(x.rows);
+      }
       if (P.hex_colored)
-        for (auto &x : colour_part(hex_pp[p], 8, p)) hex_color_pp[p].push_back((uint8_t)x.first);
+        for (auto &x : colour_part(hex_pp[p], 8, p)) hex_color_pp[p].push_back((uint8_t)x.col);
       else
         hex_color_pp[p].assign(hex_pp[p].size(), 0);
     }
+    P.tet_rows = P.colored_ok ? R_tet : 1;
   }
   // 4b. node order inside each tile by first touch: scanning the tile's
   //     batches corner by corner (corner a of every slot of the batch, then
@@ -345,7 +367,10 @@ void build_partition(const PartitionInput &in, Partition &P) {
   P.hex_slot_elem.assign(P.part_hex_start.back(), -1);
   P.tet_color.assign(P.part_tet_start.back(), 0xff);
   P.hex_color.assign(P.part_hex_start.back(), 0xff);
+  std::vector<uint8_t> tet_rowbits(P.part_tet_start.back(), 0);
   for (int p = 0; p < P.n_parts; ++p) {
+    if (P.tet_rows > 1 && p < (int)tet_rows_pp.size())
+      std::copy(tet_rows_pp[p].begin(), tet_rows_pp[p].end(), tet_rowbits.begin() + P.part_tet_start[p]);
     std::copy(tet_pp[p].begin(), tet_pp[p].end(), P.tet_slot_elem.begin() + P.part_tet_start[p]);
     std::copy(hex_pp[p].begin(), hex_pp[p].end(), P.hex_slot_elem.begin() + P.part_hex_start[p]);
     std::copy(tet_color_pp[p].begin(), tet_color_pp[p].end(), P.tet_color.begin() + P.part_tet_start[p]);
@@ -421,8 +446,10 @@ void build_partition(const PartitionInput &in, Partition &P) {
         if (n >= n0 && n < n0 + nn) return (uint16_t)(n - n0);
         return (uint16_t)(nn + hrank[std::lower_bound(halo.begin(), halo.end(), n) - halo.begin()]);
       };
+      if (P.tet_rows > 1 && nloc >= (1 << 14))
+        fail(FH_ERR_CONFIG, "tile has too many local nodes for row-tagged tet slots; lower part_nodes");
       for (int64_t q = 4 * (int64_t)P.part_tet_start[p]; q < 4 * (int64_t)(P.part_tet_start[p] + P.part_tet_count[p]); ++q)
-        P.tet_conn16[q] = local(P.tet_conn[q]);
+        P.tet_conn16[q] = (uint16_t)(local(P.tet_conn[q]) | (((tet_rowbits[q / 4] >> (2 * (q % 4))) & 3) << 14));
       for (int64_t q = 8 * (int64_t)P.part_hex_start[p]; q < 8 * (int64_t)(P.part_hex_start[p] + P.part_hex_count[p]); ++q)
         P.hex_conn16[q] = local(P.hex_conn[q]);
       P.halo_nodes.insert(P.halo_nodes.end(), hord.begin(), hord.end());

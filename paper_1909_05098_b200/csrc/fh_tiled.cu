@@ -280,12 +280,20 @@ __device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned 
   c[4] = -a + w2; c[5] = b2 + w2; c[6] = a + w2; c[7] = -b2 + w2;
 }
 
+// with accumulator rows (g.tet_rows > 1) each 16-bit word is row << 14 | local
+// index; rofs[a] = row * row_stride locates the corner's accumulator
 template <typename S, bool TD, bool LIN>
 __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned char *stage, const TK<S> *sT,
-                                          int reg, bool has_kf, int i, uint16_t nd[4], S c[4]) {
+                                          int reg, bool has_kf, int i, uint16_t nd[4], S c[4], int rofs[4],
+                                          uint32_t idx_mask, int row_stride) {
   const StageLayout<S> L(4, has_kf, g.tet_rank != nullptr, g.tet_region != nullptr);
   const uint2 w = reinterpret_cast<const uint2 *>(stage + L.conn)[i];
-  nd[0] = w.x & 0xffff; nd[1] = w.x >> 16; nd[2] = w.y & 0xffff; nd[3] = w.y >> 16;
+  const uint32_t raw[4] = {w.x & 0xffffu, w.x >> 16, w.y & 0xffffu, w.y >> 16};
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    nd[a] = (uint16_t)(raw[a] & idx_mask);
+    rofs[a] = (int)(raw[a] >> 14) * row_stride;
+  }
   S T[4], K[4];
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
@@ -402,10 +410,10 @@ __device__ __forceinline__ void accumulate(S *acc, const uint16_t (&nd)[kSPT][N]
 static_assert(kSPT == 1, "accumulate_colored handles one slot per thread");
 template <typename S, int N>
 __device__ __forceinline__ void accumulate_colored(S *acc, const uint16_t (&nd)[N], const S (&c)[N], int nfree,
-                                                   bool valid, int myph, int n_phase) {
+                                                   bool valid, int myph, int n_phase, const int *rofs = nullptr) {
   int loc[N];
 #pragma unroll
-  for (int a = 0; a < N; ++a) loc[a] = (valid && nd[a] < nfree) ? (int)nd[a] : -1;
+  for (int a = 0; a < N; ++a) loc[a] = (valid && nd[a] < nfree) ? (int)nd[a] + (rofs ? rofs[a] : 0) : -1;
   for (int ph = 0; ph < n_phase; ++ph) {
     if (myph == ph) {
 #pragma unroll
@@ -510,14 +518,15 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
     }
   }
   __syncthreads();  // every halo id has been read: the accumulators may be zeroed
-  for (int i = tid; i < (MODE == kCornerSlot ? 8 : (MODE == kCornerPhase2 ? 2 : 1)) * nfree; i += kTileThreads)
-    acc[i] = S(0);
+  const int acc_rows = max(MODE == kCornerSlot ? 8 : (MODE == kCornerPhase2 ? 2 : 1), KINDS == 2 ? 1 : g.tet_rows);
+  for (int i = tid; i < acc_rows * nfree; i += kTileThreads) acc[i] = S(0);
   __syncthreads();
 
   // uniform per launch: stage layouts and which optional streams exist
   const bool t_kf = g.tet_kf != nullptr, h_kf = g.hex_kf != nullptr;
   const bool t_reg = g.tet_region != nullptr, h_reg = g.hex_region != nullptr;
   const bool t_col = g.tet_phase != nullptr;
+  const uint32_t t_mask = g.tet_rows > 1 ? 0x3fffu : 0xffffu;  // row-tagged tet connectivity
   const StageLayout<S> Lt(4, t_kf, !t_col, t_reg);
   const StageLayout<S> Lh(8, h_kf, MODE == kRanked, h_reg);
   auto batch_nph = [&](int jj, const uint8_t *bn, int slot0) -> int {
@@ -538,13 +547,14 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       uint16_t nd[kSPT][4];
       S c[kSPT][4];
       uint8_t rk[kSPT][4];
+      int rofs[kSPT][4];
 #pragma unroll
       for (int q = 0; q < kSPT; ++q) {
         // slots past the end of a partial batch read slot 0 (always present)
         // instead of branching; only their accumulation is predicated off
         const int i = valid[q] ? q * kTileThreads + tid : 0;
         const int reg = t_reg ? (int)stage[Lt.region + i] : 0;
-        tet_loads<S, TD, LIN>(g, stage, sT, reg, t_kf, i, nd[q], c[q]);
+        tet_loads<S, TD, LIN>(g, stage, sT, reg, t_kf, i, nd[q], c[q], rofs[q], t_mask, nfree);
         // tets are never corner-unique: colour phases (phase byte per slot) or,
         // if the colouring overflowed, ranked phases (rank byte per corner)
         if (t_col) {
@@ -558,7 +568,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       }
       if (t_col)
         accumulate_colored<S, 4>(acc, nd[0], c[0], nfree, valid[0], rk[0][0],
-                                 batch_nph(j, g.tet_bnph, t_start + b * kBatch));
+                                 batch_nph(j, g.tet_bnph, t_start + b * kBatch), rofs[0]);
       else
         accumulate<S, 4, kRanked>(acc, nd, c, nfree, valid, rk, g.max_phase_tet);
     } else {
@@ -646,6 +656,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
                  ((acc[4 * nfree + loc] + acc[5 * nfree + loc]) + (acc[6 * nfree + loc] + acc[7 * nfree + loc]));
         } else if (MODE == kCornerPhase2) {
           Fsum = acc[loc] + acc[nfree + loc];
+        } else if (KINDS == 1 && g.tet_rows > 1) {  // tet accumulator rows, summed in row order
+          Fsum = (acc[loc] + acc[nfree + loc]) + (acc[2 * nfree + loc] + acc[3 * nfree + loc]);
         } else {
           Fsum = acc[loc];
         }

@@ -38,7 +38,7 @@ class Plan:
 
     INFO = ("n_parts", "rank_parts", "boundary_parts", "n_peers", "n_send", "n_recv", "node_lo", "node_hi",
             "corner_unique", "max_phase_tet", "max_phase_hex", "n_slots", "max_local_nodes", "colored_ok",
-            "max_colors", "max_nph_tet", "max_nph_hex")
+            "max_colors", "max_nph_tet", "max_nph_hex", "sum_nph_tet", "nph_len_tet", "sum_nph_hex", "nph_len_hex")
 
     def __init__(self, mesh, material, boundary: BoundarySpec | None = None, *, world: int = 1, rank: int = 0,
                  n_domains: int = DEFAULT_DOMAINS, slab_axis: int = -1, part_nodes: int = 0, precision: int = 32,

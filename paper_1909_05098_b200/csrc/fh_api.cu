@@ -531,7 +531,8 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   if (const char *env = getenv("FH_TILE_MODE")) {
     const int m = atoi(env);
     if (m == kModeRanked || m == kModeSharedAtomic || (m == kModeColored && hex_colour_ok) ||
-        ((m == kModeCornerPhase || m == kModeCornerSlot || m == kModeCornerPhase2) && P.corner_unique))
+        ((m == kModeCornerPhase || m == kModeCornerSlot || m == kModeCornerPhase2 || m == kModeCornerPhase4) &&
+         P.corner_unique))
       mode = m;
   }
   // `mode` is the hex mode (kernel template); tets never are corner-unique and
@@ -691,7 +692,9 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   if (const char *env = getenv("FH_TILE_STAGES")) g.n_stages = std::min(kMaxStages, std::max(1, atoi(env)));
   g.smem_T = (int)al(2 * sizeof(S) * (size_t)std::max(1, P.max_local_nodes));
   // +1: the trash slot of the corner-phase accumulation
-  const int rows = std::max(st->mode == kModeCornerSlot ? 8 : (st->mode == kModeCornerPhase2 ? 2 : 1), P.tet_rows);
+  const int rows = std::max(st->mode == kModeCornerSlot ? 8 : st->mode == kModeCornerPhase4 ? 4
+                                                            : (st->mode == kModeCornerPhase2 ? 2 : 1),
+                            P.tet_rows);
   g.smem_acc = (int)al(sizeof(S) * rows * ((size_t)std::max(1, P.max_part_free) + 1));
   {  // the accumulator region first holds the tile's halo id list (bulk copy)
     int max_halo = 0;

@@ -333,7 +333,10 @@ __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned 
 //                but the summation order is not fixed (tolerance-only, opt-in)
 //   kCornerPhase2  corner phases with two accumulator rows (corners a and
 //                a + N/2 share a phase): half the barriers, 2x accumulator smem
-enum { kRanked = 0, kCornerPhase = 1, kCornerSlot = 2, kColored = 3, kSharedAtomic = 4, kCornerPhase2 = 5 };
+//   kCornerPhase4  corner phases with four accumulator rows (corners a, a+1,
+//                a+2, a+3 of one half share a phase): 2 barriers, 4x smem
+enum { kRanked = 0, kCornerPhase = 1, kCornerSlot = 2, kColored = 3, kSharedAtomic = 4, kCornerPhase2 = 5,
+       kCornerPhase4 = 6 };
 
 template <typename S, int N, int MODE>
 __device__ __forceinline__ void accumulate(S *acc, const uint16_t (&nd)[kSPT][N], const S (&c)[kSPT][N], int nfree,
@@ -369,6 +372,18 @@ __device__ __forceinline__ void accumulate(S *acc, const uint16_t (&nd)[kSPT][N]
         if (loc[q][a] >= 0) acc[loc[q][a]] -= c[q][a];
         if (loc[q][a + N / 2] >= 0) acc1[loc[q][a + N / 2]] -= c[q][a + N / 2];
       }
+      __syncthreads();
+    }
+  } else if (MODE == kCornerPhase4) {
+    // four rows: corner h * N/2 + r into row r, one phase per half -> 2 barriers
+    // per hex batch; F = (row0 + row1) + (row2 + row3)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int q = 0; q < kSPT; ++q)
+#pragma unroll
+        for (int r = 0; r < N / 2; ++r)
+          if (loc[q][h * (N / 2) + r] >= 0) acc[r * nfree + loc[q][h * (N / 2) + r]] -= c[q][h * (N / 2) + r];
       __syncthreads();
     }
   } else if (MODE == kCornerPhase && !FH_TRASH_SLOT) {
@@ -518,7 +533,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
     }
   }
   __syncthreads();  // every halo id has been read: the accumulators may be zeroed
-  const int acc_rows = max(MODE == kCornerSlot ? 8 : (MODE == kCornerPhase2 ? 2 : 1), KINDS == 2 ? 1 : g.tet_rows);
+  const int acc_rows = max(MODE == kCornerSlot ? 8 : (MODE == kCornerPhase4 ? 4 : (MODE == kCornerPhase2 ? 2 : 1)),
+                           KINDS == 2 ? 1 : g.tet_rows);
   for (int i = tid; i < acc_rows * nfree; i += kTileThreads) acc[i] = S(0);
   __syncthreads();
 
@@ -656,6 +672,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
                  ((acc[4 * nfree + loc] + acc[5 * nfree + loc]) + (acc[6 * nfree + loc] + acc[7 * nfree + loc]));
         } else if (MODE == kCornerPhase2) {
           Fsum = acc[loc] + acc[nfree + loc];
+        } else if (MODE == kCornerPhase4 && KINDS != 1) {
+          Fsum = (acc[loc] + acc[nfree + loc]) + (acc[2 * nfree + loc] + acc[3 * nfree + loc]);
         } else if (KINDS == 1 && g.tet_rows > 1) {  // tet accumulator rows, summed in row order
           Fsum = (acc[loc] + acc[nfree + loc]) + (acc[2 * nfree + loc] + acc[3 * nfree + loc]);
         } else {
@@ -717,23 +735,25 @@ void tiled_step(const TiledArgs<S> &g, int n_parts, bool td, int mode_sel, size_
 #define FH_MODES(TDV, KV, L)                                                                       \
   {k_tiled_step<S, TDV, kRanked, KV, L>, k_tiled_step<S, TDV, kCornerPhase, KV, L>,                 \
    k_tiled_step<S, TDV, kCornerSlot, KV, L>, k_tiled_step<S, TDV, kColored, KV, L>,                 \
-   k_tiled_step<S, TDV, kSharedAtomic, KV, L>, k_tiled_step<S, TDV, kCornerPhase2, KV, L>}
+   k_tiled_step<S, TDV, kSharedAtomic, KV, L>, k_tiled_step<S, TDV, kCornerPhase2, KV, L>,          \
+   k_tiled_step<S, TDV, kCornerPhase4, KV, L>}
 #define FH_TETONLY(TDV, L)                                                                         \
   {k_tiled_step<S, TDV, kRanked, 1, L>, k_tiled_step<S, TDV, kRanked, 1, L>,                        \
    k_tiled_step<S, TDV, kRanked, 1, L>, k_tiled_step<S, TDV, kRanked, 1, L>,                        \
-   k_tiled_step<S, TDV, kRanked, 1, L>, k_tiled_step<S, TDV, kRanked, 1, L>}
-  static const K table[2][2][3][6] = {
+   k_tiled_step<S, TDV, kRanked, 1, L>, k_tiled_step<S, TDV, kRanked, 1, L>,                        \
+   k_tiled_step<S, TDV, kRanked, 1, L>}
+  static const K table[2][2][3][7] = {
       {{FH_MODES(false, 0, false), FH_TETONLY(false, false), FH_MODES(false, 2, false)},
        {FH_MODES(true, 0, false), FH_TETONLY(true, false), FH_MODES(true, 2, false)}},
       {{FH_MODES(false, 0, false), FH_TETONLY(false, false), FH_MODES(false, 2, false)},
        {FH_MODES(true, 0, true), FH_TETONLY(true, true), FH_MODES(true, 2, true)}}};
 #undef FH_MODES
 #undef FH_TETONLY
-  const int mode = mode_sel < 0 || mode_sel > 5 ? 0 : mode_sel;
+  const int mode = mode_sel < 0 || mode_sel > 6 ? 0 : mode_sel;
   const int kinds = (g.tet_rec && g.hex_rec) ? 2 : (g.hex_rec ? 0 : 1);
   const int lin = g.lin ? 1 : 0;
   const K kern = table[lin][td ? 1 : 0][kinds][mode];
-  static size_t configured[2][2][3][6] = {};
+  static size_t configured[2][2][3][7] = {};
   size_t &cfg = configured[lin][td ? 1 : 0][kinds][mode];
   if (smem > cfg) {
     FH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

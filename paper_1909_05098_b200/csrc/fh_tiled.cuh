@@ -94,7 +94,8 @@ enum TileMode {
   kModeCornerSlot = 2,
   kModeColored = 3,
   kModeSharedAtomic = 4,
-  kModeCornerPhase2 = 5
+  kModeCornerPhase2 = 5,
+  kModeCornerPhase4 = 6
 };
 
 // TI freeze: per-slot kbar (global-id connectivity conn4/conn8) and per-node

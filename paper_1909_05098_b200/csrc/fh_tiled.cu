@@ -498,38 +498,45 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
     prefetch_range(g.q_ext ? g.q_ext + n0 : nullptr, sizeof(S) * nfree);
 #endif
   }
-  // stage temperatures: owned range + halo list; zero accumulators
-  const bool kstage = TD;  // k of material 0 (other materials interpolate per slot)
+  // stage temperatures: owned range + halo list; zero accumulators.  Loads
+  // are clamped to valid addresses and only the shared stores are predicated,
+  // so the unrolled rounds stay branch-free; k(T) of material 0 comes from a
+  // two-knot law held in registers (LIN) -- other materials interpolate per slot.
+  const bool kstage = TD;
   const Curve<S> &k0 = g.mats.m[0].k;
+  const S kx0 = k0.x[0], kx1 = k0.x[1], ky0 = k0.y[0], ky1 = k0.y[1], ks = k0.slope[0];
+  auto k_of = [&](S x) -> S {
+    if (!kstage) return S(0);
+    if (!LIN) return interp(k0, x);
+    S r = ks * (x - kx0) + ky0;  // == ip<true>(k0, x), operation for operation
+    r = (x >= kx1) ? ky1 : r;
+    return (x <= kx0) ? ky0 : r;
+  };
   constexpr int U = FH_STAGE_UNROLL;  // loads in flight per thread while staging
   for (int base = tid; base < nn; base += U * kTileThreads) {
     S x[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = base + u * kTileThreads;
-      x[u] = i < nn ? __ldg(g.Tin + n0 + i) : S(0);
-    }
+    for (int u = 0; u < U; ++u) x[u] = __ldg(g.Tin + n0 + min(base + u * kTileThreads, nn - 1));
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = base + u * kTileThreads;
-      if (i < nn) sT[i] = TK<S>{x[u], kstage ? ip<LIN>(k0, x[u]) : S(0)};
+      const TK<S> v{x[u], k_of(x[u])};
+      if (i < nn) sT[i] = v;
     }
   }
   mbar_wait(&hbar, 0);
   for (int base = tid; base < nh; base += U * kTileThreads) {
     int id[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = base + u * kTileThreads;
-      id[u] = i < nh ? s_ids[hoff + i] : 0;
-    }
+    for (int u = 0; u < U; ++u) id[u] = s_ids[hoff + min(base + u * kTileThreads, nh - 1)];
     S x[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) x[u] = __ldg(g.Tin + id[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = base + u * kTileThreads;
-      if (i < nh) sT[nn + i] = TK<S>{x[u], kstage ? ip<LIN>(k0, x[u]) : S(0)};
+      const TK<S> v{x[u], k_of(x[u])};
+      if (i < nh) sT[nn + i] = v;
     }
   }
   __syncthreads();  // every halo id has been read: the accumulators may be zeroed

@@ -194,6 +194,17 @@ int fh_step_timed_flush(fh_engine *e, int64_t nsteps, double dt, void *scratch, 
 int fh_step_host(fh_engine *e, const double *T_in, double *T_out, int64_t n, int64_t nsteps, double dt,
                  fh_report *rep);
 
+/* fh_step_host, double-buffered (single GPU).  Queues: upload T_in into the
+ * device staging field of `slot` (0 or 1) on a copy stream, nsteps steps on
+ * the engine stream, download of the new field into T_out on a second copy
+ * stream; returns without waiting.  T_in / T_out must be pinned and stay
+ * untouched until fh_host_wait(slot).  Alternating slots lets the upload of
+ * call k+1 and the download of call k share the bus in both directions.  A
+ * runaway step is reported by fh_host_wait (FH_ERR_INSTABILITY, fail_step). */
+int fh_step_host_async(fh_engine *e, const double *T_in, double *T_out, int64_t n, int64_t nsteps, double dt,
+                       int32_t slot);
+int fh_host_wait(fh_engine *e, int32_t slot, fh_report *rep);
+
 /* set the static extra nodal power (W, original numbering, n == V) */
 int fh_set_q_static(fh_engine *e, const double *q, int64_t n);
 

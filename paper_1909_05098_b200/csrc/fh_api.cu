@@ -216,8 +216,21 @@ struct fh_engine {
   std::vector<int64_t> probe_steps;
   // critical dt scratch
   DBuf<double> crit_kbar, crit_lam;
+  // double-buffered host I/O (fh_step_host_async / fh_host_wait): per slot an
+  // input and an output staging field, copy streams in each direction
+  DBuf<double> io_in[2], io_out[2];
+  cudaStream_t io_h2d = nullptr, io_d2h = nullptr;
+  cudaEvent_t io_ev[2][4] = {};  // in ready, in consumed, out ready, out copied
+  bool io_used[2] = {false, false};
+  FailFlag *io_flag = nullptr;  // pinned: the fail flag after each slot's steps
 
   ~fh_engine() {
+    if (io_flag) cudaFreeHost(io_flag);
+    for (auto &evs : io_ev)
+      for (cudaEvent_t ev : evs)
+        if (ev) cudaEventDestroy(ev);
+    if (io_h2d) cudaStreamDestroy(io_h2d);
+    if (io_d2h) cudaStreamDestroy(io_d2h);
     if (comm) nccl_comm_destroy(comm);
     if (ev_packed) cudaEventDestroy(ev_packed);
     if (ev_halo) cudaEventDestroy(ev_halo);
@@ -719,7 +732,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
 }
 
 template <typename S>
-void tiled_set_T(fh_engine *e) {  // e->stage holds the field in original order
+void tiled_set_T(fh_engine *e, const double *src = nullptr) {  // src (default e->stage): original order
   TiledState<S> &st = tstate<S>(e);
   float *f0 = nullptr, *f1 = nullptr;
   double *d0 = nullptr, *d1 = nullptr;
@@ -730,7 +743,7 @@ void tiled_set_T(fh_engine *e) {  // e->stage holds the field in original order
     d0 = st.T[0].p;
     d1 = st.T[1].p;
   }
-  k_to_new<<<nblk(e->V), kBlk, 0, e->stream>>>(e->stage.p, e->old_of_new.p, e->V, f0, d0, f1, d1);
+  k_to_new<<<nblk(e->V), kBlk, 0, e->stream>>>(src ? src : e->stage.p, e->old_of_new.p, e->V, f0, d0, f1, d1);
   FH_CUDA(cudaGetLastError());
   st.cur = 0;
 }
@@ -742,14 +755,15 @@ void tiled_get_T(fh_engine *e, double *dst_dev) {
   FH_CUDA(cudaGetLastError());
 }
 
-// current field, original order, fp64, into e->stage (device)
-void current_T_to_stage(fh_engine *e) {
+// current field, original order, fp64, into dst (default e->stage; device)
+void current_T_to_stage(fh_engine *e, double *dst = nullptr) {
+  double *d = dst ? dst : e->stage.p;
   if (e->assembly == FH_ASSEMBLY_EXACT) {
-    FH_CUDA(cudaMemcpyAsync(e->stage.p, e->T.p, sizeof(double) * e->V, cudaMemcpyDeviceToDevice, e->stream));
+    FH_CUDA(cudaMemcpyAsync(d, e->T.p, sizeof(double) * e->V, cudaMemcpyDeviceToDevice, e->stream));
   } else if (e->precision == 32) {
-    tiled_get_T<float>(e, e->stage.p);
+    tiled_get_T<float>(e, d);
   } else {
-    tiled_get_T<double>(e, e->stage.p);
+    tiled_get_T<double>(e, d);
   }
 }
 
@@ -1221,6 +1235,78 @@ int fh_step_timed_flush(fh_engine *e, int64_t nsteps, double dt, void *scratch, 
   check_engine(e);
   if (!scratch || !scratch_bytes) fail(FH_ERR_CONFIG, "scratch buffer required");
   return do_step(e, nsteps, dt, rep, elapsed_ms, scratch, scratch_bytes);
+  FH_API_END
+}
+
+int fh_step_host_async(fh_engine *e, const double *T_in, double *T_out, int64_t n, int64_t nsteps, double dt,
+                       int32_t slot) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (n != e->V) fail(FH_ERR_CONFIG, "field has the wrong length");
+  if (slot < 0 || slot > 1) fail(FH_ERR_CONFIG, "slot must be 0 or 1");
+  if (e->comm) fail(FH_ERR_CONFIG, "fh_step_host_async is single-GPU only");
+  if (nsteps < 0) fail(FH_ERR_CONFIG, "nsteps must be >= 0");
+  if (!(dt > 0.0) || !std::isfinite(dt)) fail(FH_ERR_CONFIG, "dt must be positive and finite");
+  if (e->io_used[slot]) fail(FH_ERR_CONFIG, "slot still in flight: call fh_host_wait first");
+  if (!e->io_h2d) {
+    FH_CUDA(cudaStreamCreateWithFlags(&e->io_h2d, cudaStreamNonBlocking));
+    FH_CUDA(cudaStreamCreateWithFlags(&e->io_d2h, cudaStreamNonBlocking));
+    for (auto &evs : e->io_ev)
+      for (cudaEvent_t &ev : evs) FH_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    FH_CUDA(cudaMallocHost(reinterpret_cast<void **>(&e->io_flag), 2 * sizeof(FailFlag)));
+  }
+  cudaEvent_t *ev = e->io_ev[slot];
+  if (!e->io_in[slot].p) {
+    e->io_in[slot].alloc(e->V);
+    e->io_out[slot].alloc(e->V);
+    for (int k = 0; k < 4; ++k) FH_CUDA(cudaEventRecord(ev[k], e->stream));  // all free
+  }
+  // upload on its own stream once the slot's previous field was consumed
+  FH_CUDA(cudaStreamWaitEvent(e->io_h2d, ev[1], 0));
+  FH_CUDA(cudaMemcpyAsync(e->io_in[slot].p, T_in, sizeof(double) * e->V, cudaMemcpyHostToDevice, e->io_h2d));
+  FH_CUDA(cudaEventRecord(ev[0], e->io_h2d));
+  // compute stream: field in, steps, field out (into the slot's output buffer
+  // once its previous download finished)
+  FH_CUDA(cudaStreamWaitEvent(e->stream, ev[0], 0));
+  if (e->assembly == FH_ASSEMBLY_EXACT)
+    FH_CUDA(cudaMemcpyAsync(e->T.p, e->io_in[slot].p, sizeof(double) * e->V, cudaMemcpyDeviceToDevice, e->stream));
+  else if (e->precision == 32)
+    tiled_set_T<float>(e, e->io_in[slot].p);
+  else
+    tiled_set_T<double>(e, e->io_in[slot].p);
+  FH_CUDA(cudaEventRecord(ev[1], e->stream));
+  run_steps(e, nsteps, dt);
+  FH_CUDA(cudaMemcpyAsync(&e->io_flag[slot], e->flag.p, sizeof(FailFlag), cudaMemcpyDeviceToHost, e->stream));
+  FH_CUDA(cudaStreamWaitEvent(e->stream, ev[3], 0));
+  current_T_to_stage(e, e->io_out[slot].p);
+  FH_CUDA(cudaEventRecord(ev[2], e->stream));
+  // download on its own stream: overlaps the next call's upload and steps
+  FH_CUDA(cudaStreamWaitEvent(e->io_d2h, ev[2], 0));
+  FH_CUDA(cudaMemcpyAsync(T_out, e->io_out[slot].p, sizeof(double) * e->V, cudaMemcpyDeviceToHost, e->io_d2h));
+  FH_CUDA(cudaEventRecord(ev[3], e->io_d2h));
+  e->io_used[slot] = true;
+  FH_API_END
+}
+
+int fh_host_wait(fh_engine *e, int32_t slot, fh_report *rep) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (slot < 0 || slot > 1 || !e->io_used[slot]) fail(FH_ERR_CONFIG, "slot is not in flight");
+  FH_CUDA(cudaEventSynchronize(e->io_ev[slot][3]));  // ordered after the flag copy
+  e->io_used[slot] = false;
+  const FailFlag f = e->io_flag[slot];
+  if (rep) {
+    std::memset(rep, 0, sizeof(*rep));
+    rep->fail_step = -1;
+    rep->fail_node = -1;
+    rep->time = e->time;
+    rep->step_index = e->step_index;
+  }
+  if (f.step != ~0ull) {
+    if (rep) rep->fail_step = (int64_t)f.step;
+    fail(FH_ERR_INSTABILITY, "step " + std::to_string((int64_t)f.step) +
+                                 ": non-finite or runaway temperature (fh_step_host_async)");
+  }
   FH_API_END
 }
 

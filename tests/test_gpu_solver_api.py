@@ -208,3 +208,46 @@ def test_full_runs_bitwise_repeatable(assembly, prec):
     a = eng.run(37.0, steps=60, dt=0.01).state.temperatures
     b = eng.run(37.0, steps=60, dt=0.01).state.temperatures
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("assembly,prec", [("exact", 64), ("tiled", 32)])
+def test_step_host_async_matches_sync(assembly, prec):
+    """fh_step_host_async (double-buffered host I/O) == fh_step_host, bitwise,
+    for alternating slots; misuse (slot still in flight) is a ConfigError."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1909_05098_b200 import _native as N
+
+    mesh = fh.generate_cube_mesh("hex", 8, 0.1)
+    mat = fh.TissueMaterial(density=fh.make_constant(1060.0), specific_heat=fh.linear_law(3600.0, -0.0005, 37.0),
+                            conductivity=fh.linear_law(0.5, 0.0013, 37.0), perfusion_rate=0.525,
+                            blood_specific_heat=3640.0, metabolic_rate=420.0)
+    bnd = fh.BoundarySpec(dirichlet=(("z0", 37.0),), heat_loads=(("center", 0.5, 0.0, 1e9),))
+    eng = fh.ExplicitEngine(mesh, mat, bnd, assembly=assembly, precision=prec)
+    dt = 0.9 * eng.critical_dt(37.0)
+    L, h, V = eng._L, eng._h, mesh.n_nodes
+    rng = np.random.default_rng(7)
+    fields = [37.0 + rng.random(V) for _ in range(4)]
+    rep = N.FhReport()
+    ref = []
+    for f in fields:
+        out = np.empty(V)
+        N.check(L.fh_step_host(h, N.ptr(np.ascontiguousarray(f)), N.ptr(out), V, 3, dt, C.byref(rep)))
+        ref.append(out)
+    pins = [torch.empty(V, dtype=torch.float64, pin_memory=True) for _ in range(4)]
+    outs = [torch.empty(V, dtype=torch.float64, pin_memory=True) for _ in range(4)]
+    ptr = lambda t: C.cast(C.c_void_p(t.data_ptr()), N.f64p)  # noqa: E731
+    for k, f in enumerate(fields):
+        pins[k].numpy()[:] = f
+        N.check(L.fh_step_host_async(h, ptr(pins[k]), ptr(outs[k]), V, 3, dt, k % 2))
+        if k >= 1:
+            N.check(L.fh_host_wait(h, (k - 1) % 2, C.byref(rep)))
+    N.check(L.fh_host_wait(h, 1, C.byref(rep)))
+    for k in range(4):
+        assert np.array_equal(outs[k].numpy(), ref[k])
+    N.check(L.fh_step_host_async(h, ptr(pins[0]), ptr(outs[0]), V, 1, dt, 0))
+    with pytest.raises(fh.ConfigError):
+        N.check(L.fh_step_host_async(h, ptr(pins[1]), ptr(outs[1]), V, 1, dt, 0))
+    N.check(L.fh_host_wait(h, 0, C.byref(rep)))

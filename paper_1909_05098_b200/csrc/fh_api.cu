@@ -151,6 +151,7 @@ struct TiledState {
   DBuf<S> tet_kf, hex_kf, tet_kbar, hex_kbar;
   DBuf<uint8_t> tet_rank, hex_rank, tet_region, hex_region, node_region;
   DBuf<int8_t> part_mat;
+  bool nph_packed = false;
   DBuf<uint8_t> tet_phase, hex_phase, tet_bnph, hex_bnph;
   DBuf<S> T[2], vol, cap, kb, q_ext, xyz, robin_hA, robin_hAT;
   int cur = 0;
@@ -553,12 +554,22 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   const int tet_mode = P.colored_ok ? kModeColored : kModeRanked;
   if (mode == kModeRanked) st->hex_rank.upload(P.hex_rank, s);
   if (tet_mode == kModeRanked) st->tet_rank.upload(P.tet_rank, s);
+  // colour phase bytes: phase in the low nibble and, when every batch has at
+  // most 15 phases, the batch's phase count in the high nibble (the kernel
+  // then reads both from the slot's own byte)
+  st->nph_packed = P.max_nph_tet <= 15 && P.max_nph_hex <= 15;
+  auto pack_phases = [&](const std::vector<uint8_t> &phase, const std::vector<uint8_t> &bnph) {
+    std::vector<uint8_t> out(phase);
+    if (st->nph_packed)
+      for (size_t q = 0; q < out.size(); ++q) out[q] = (uint8_t)(out[q] | (bnph[q / kBatch] << 4));
+    return out;
+  };
   if (mode == kModeColored) {
-    st->hex_phase.upload(P.hex_phase, s);
+    st->hex_phase.upload(pack_phases(P.hex_phase, P.hex_batch_nph), s);
     st->hex_bnph.upload(P.hex_batch_nph, s);
   }
   if (tet_mode == kModeColored) {
-    st->tet_phase.upload(P.tet_phase, s);
+    st->tet_phase.upload(pack_phases(P.tet_phase, P.tet_batch_nph), s);
     st->tet_bnph.upload(P.tet_batch_nph, s);
   }
   const int64_t nts = (int64_t)P.tet_slot_elem.size(), nhs = (int64_t)P.hex_slot_elem.size();
@@ -693,6 +704,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.mats = mats_of<S>(e);
   g.lin = normalise_curves(g.mats);
   g.tet_rows = P.tet_rows;
+  g.nph_packed = st->nph_packed ? 1 : 0;
   g.n_src = 0;  // set per step from the active sources
   g.n_gauss = 0;
   g.runaway_limit = (S)e->runaway_limit;

@@ -571,6 +571,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       S c[kSPT][4];
       uint8_t rk[kSPT][4];
       int rofs[kSPT][4];
+      int t_nph = 0;
 #pragma unroll
       for (int q = 0; q < kSPT; ++q) {
         // slots past the end of a partial batch read slot 0 (always present)
@@ -581,7 +582,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         // tets are never corner-unique: colour phases (phase byte per slot) or,
         // if the colouring overflowed, ranked phases (rank byte per corner)
         if (t_col) {
-          const uint8_t ph = stage[Lt.phase + i];
+          const uint8_t pb = stage[Lt.phase + i];
+          t_nph = pb >> 4;
+          const uint8_t ph = g.nph_packed ? (uint8_t)(pb & 15) : pb;
 #pragma unroll
           for (int a = 0; a < 4; ++a) rk[q][a] = ph;
         } else {
@@ -591,13 +594,14 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       }
       if (t_col)
         accumulate_colored<S, 4>(acc, nd[0], c[0], nfree, valid[0], rk[0][0],
-                                 batch_nph(j, g.tet_bnph, t_start + b * kBatch), rofs[0]);
+                                 g.nph_packed ? t_nph : batch_nph(j, g.tet_bnph, t_start + b * kBatch), rofs[0]);
       else
         accumulate<S, 4, kRanked>(acc, nd, c, nfree, valid, rk, g.max_phase_tet);
     } else {
       uint16_t nd[kSPT][8];
       S c[kSPT][8];
       uint8_t rk[kSPT][8];
+      int h_nph = 0;
 #pragma unroll
       for (int q = 0; q < kSPT; ++q) {
         const int i = valid[q] ? q * kTileThreads + tid : 0;
@@ -611,7 +615,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
             rk[q][a + 4] = (w.y >> (8 * a)) & 0xff;
           }
         } else if (MODE == kColored) {
-          const uint8_t ph = stage[Lh.phase + i];
+          const uint8_t pb = stage[Lh.phase + i];
+          h_nph = pb >> 4;
+          const uint8_t ph = g.nph_packed ? (uint8_t)(pb & 15) : pb;
 #pragma unroll
           for (int a = 0; a < 8; ++a) rk[q][a] = ph;
         } else {
@@ -621,7 +627,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       }
       if (MODE == kColored)
         accumulate_colored<S, 8>(acc, nd[0], c[0], nfree, valid[0], rk[0][0],
-                                 batch_nph(j, g.hex_bnph, h_start + b * kBatch));
+                                 g.nph_packed ? h_nph : batch_nph(j, g.hex_bnph, h_start + b * kBatch));
       else
         accumulate<S, 8, MODE>(acc, nd, c, nfree, valid, rk, g.max_phase_hex);
     }

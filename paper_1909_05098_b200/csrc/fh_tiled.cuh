@@ -56,6 +56,7 @@ struct TiledArgs {
   MatSet<S> mats;   // one-knot curves normalised to two knots (see normalise_curves)
   int lin;          // every curve has <= 2 knots: branch-free interpolation kernels
   int tet_rows;     // tet accumulator rows (1 or 4; tet-only meshes), see Partition::tet_rows
+  int nph_packed;   // phase bytes carry the batch's phase count in their high nibble
   int n_gauss;      // active sources, Gaussians first: src[0, n_gauss) Gaussian, [n_gauss, n_src) RF
   int n_src;
   SourceT<S> src[kMaxSources];

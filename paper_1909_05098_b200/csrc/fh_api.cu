@@ -151,7 +151,6 @@ struct TiledState {
   DBuf<S> tet_kf, hex_kf, tet_kbar, hex_kbar;
   DBuf<uint8_t> tet_rank, hex_rank, tet_region, hex_region, node_region;
   DBuf<int8_t> part_mat;
-  bool nph_packed = false;
   DBuf<uint8_t> tet_phase, hex_phase, tet_bnph, hex_bnph;
   DBuf<S> T[2], vol, cap, kb, q_ext, xyz, robin_hA, robin_hAT;
   int cur = 0;
@@ -224,6 +223,7 @@ struct fh_engine {
   cudaEvent_t io_ev[2][4] = {};  // in ready, in consumed, out ready, out copied
   bool io_used[2] = {false, false};
   FailFlag *io_flag = nullptr;  // pinned: the fail flag after each slot's steps
+  int refit_per_sm = 0;          // wave fit: measured resident step CTAs per SM (second pass)
 
   ~fh_engine() {
     if (io_flag) cudaFreeHost(io_flag);
@@ -297,14 +297,15 @@ int default_tet_rows(int64_t n_tet, int64_t n_hex) {
 // (cfg3: 1480 tiles, 0.0923 -> 0.089 ms/step; scripts/sweep.py).  Parts per
 // domain are ceil(V_domain / target) (fh_partition.cpp), so the count is exact.
 int wave_fit_part_nodes(int target, int64_t V, int n_domains, int precision, int64_t n_tet, int64_t n_hex,
-                        int device) {
+                        int device, int per_sm_measured = 0) {
   int sms = 148;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || sms <= 0) {
     cudaGetLastError();
     sms = 148;
   }
   // resident step CTAs per SM (the launch bounds of k_tiled_step)
-  const int per_sm = precision != 32 ? 2 : (n_hex == 0 ? 5 : 4);
+  // (the launch bounds' minimum; setup_tiled refits with the measured value)
+  const int per_sm = per_sm_measured > 0 ? per_sm_measured : (precision != 32 ? 2 : (n_hex == 0 ? 5 : 4));
   const int64_t cap = (int64_t)sms * per_sm;
   const int64_t vd = (V + n_domains - 1) / n_domains;
   const int64_t n0 = (int64_t)n_domains * ((vd + target - 1) / target);
@@ -471,7 +472,9 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     pin.target_part_nodes = (int)std::max<int64_t>(96, V / (2 * 148));
   else if (o.part_nodes <= 0)
     pin.target_part_nodes = wave_fit_part_nodes(pin.target_part_nodes, V, std::max(1, o.n_domains),
-                                                sizeof(S) == 4 ? 32 : 64, e->n_tet, e->n_hex, o.device);
+                                                sizeof(S) == 4 ? 32 : 64, e->n_tet, e->n_hex, o.device,
+                                                e->refit_per_sm);
+  const int target_used = pin.target_part_nodes;
   pin.batch = kBatch;
   // layout tuning knobs (scripts/sweep.py): hex colour order, first-touch node order
   if (const char *env = getenv("FH_HEX_COLOR")) pin.hex_color = atoi(env);
@@ -554,22 +557,12 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   const int tet_mode = P.colored_ok ? kModeColored : kModeRanked;
   if (mode == kModeRanked) st->hex_rank.upload(P.hex_rank, s);
   if (tet_mode == kModeRanked) st->tet_rank.upload(P.tet_rank, s);
-  // colour phase bytes: phase in the low nibble and, when every batch has at
-  // most 15 phases, the batch's phase count in the high nibble (the kernel
-  // then reads both from the slot's own byte)
-  st->nph_packed = P.max_nph_tet <= 15 && P.max_nph_hex <= 15;
-  auto pack_phases = [&](const std::vector<uint8_t> &phase, const std::vector<uint8_t> &bnph) {
-    std::vector<uint8_t> out(phase);
-    if (st->nph_packed)
-      for (size_t q = 0; q < out.size(); ++q) out[q] = (uint8_t)(out[q] | (bnph[q / kBatch] << 4));
-    return out;
-  };
   if (mode == kModeColored) {
-    st->hex_phase.upload(pack_phases(P.hex_phase, P.hex_batch_nph), s);
+    st->hex_phase.upload(P.hex_phase, s);
     st->hex_bnph.upload(P.hex_batch_nph, s);
   }
   if (tet_mode == kModeColored) {
-    st->tet_phase.upload(pack_phases(P.tet_phase, P.tet_batch_nph), s);
+    st->tet_phase.upload(P.tet_phase, s);
     st->tet_bnph.upload(P.tet_batch_nph, s);
   }
   const int64_t nts = (int64_t)P.tet_slot_elem.size(), nhs = (int64_t)P.hex_slot_elem.size();
@@ -704,7 +697,6 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.mats = mats_of<S>(e);
   g.lin = normalise_curves(g.mats);
   g.tet_rows = P.tet_rows;
-  g.nph_packed = st->nph_packed ? 1 : 0;
   g.n_src = 0;  // set per step from the active sources
   g.n_gauss = 0;
   g.runaway_limit = (S)e->runaway_limit;
@@ -736,6 +728,20 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.stage_bytes = (int)al(stage);
   st->smem = (size_t)g.smem_T + g.smem_acc + (size_t)g.n_stages * g.stage_bytes;
   if (st->smem > 220 * 1024) fail(FH_ERR_CONFIG, "tile too large for shared memory; lower part_nodes");
+  // wave fit, second pass: the first pass assumed the launch bounds' CTAs per
+  // SM; if the kernel actually keeps a different number resident at this
+  // shared memory size (fp64 tiles), partition again for that count
+  if (o.part_nodes <= 0 && e->refit_per_sm == 0 && !(V / target_used < 2 * 148)) {
+    const int bps = tiled_occupancy<S>(g, e->td, mode, st->smem);
+    if (bps > 0 && wave_fit_part_nodes(default_part_nodes(sizeof(S) == 4 ? 32 : 64, e->n_tet, e->n_hex), V,
+                                       std::max(1, o.n_domains), sizeof(S) == 4 ? 32 : 64, e->n_tet, e->n_hex,
+                                       o.device, bps) != target_used) {
+      e->refit_per_sm = bps;
+      FH_CUDA(cudaStreamSynchronize(s));
+      setup_tiled<S>(e, mesh, b, G_dev);  // replaces the partition and every tiled buffer
+      return;
+    }
+  }
   FH_CUDA(cudaStreamSynchronize(s));
   if constexpr (sizeof(S) == 4)
     e->tf = std::move(st);

@@ -571,7 +571,6 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       S c[kSPT][4];
       uint8_t rk[kSPT][4];
       int rofs[kSPT][4];
-      int t_nph = 0;
 #pragma unroll
       for (int q = 0; q < kSPT; ++q) {
         // slots past the end of a partial batch read slot 0 (always present)
@@ -582,9 +581,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         // tets are never corner-unique: colour phases (phase byte per slot) or,
         // if the colouring overflowed, ranked phases (rank byte per corner)
         if (t_col) {
-          const uint8_t pb = stage[Lt.phase + i];
-          t_nph = pb >> 4;
-          const uint8_t ph = g.nph_packed ? (uint8_t)(pb & 15) : pb;
+          const uint8_t ph = stage[Lt.phase + i];
 #pragma unroll
           for (int a = 0; a < 4; ++a) rk[q][a] = ph;
         } else {
@@ -594,14 +591,13 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       }
       if (t_col)
         accumulate_colored<S, 4>(acc, nd[0], c[0], nfree, valid[0], rk[0][0],
-                                 g.nph_packed ? t_nph : batch_nph(j, g.tet_bnph, t_start + b * kBatch), rofs[0]);
+                                 batch_nph(j, g.tet_bnph, t_start + b * kBatch), rofs[0]);
       else
         accumulate<S, 4, kRanked>(acc, nd, c, nfree, valid, rk, g.max_phase_tet);
     } else {
       uint16_t nd[kSPT][8];
       S c[kSPT][8];
       uint8_t rk[kSPT][8];
-      int h_nph = 0;
 #pragma unroll
       for (int q = 0; q < kSPT; ++q) {
         const int i = valid[q] ? q * kTileThreads + tid : 0;
@@ -615,9 +611,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
             rk[q][a + 4] = (w.y >> (8 * a)) & 0xff;
           }
         } else if (MODE == kColored) {
-          const uint8_t pb = stage[Lh.phase + i];
-          h_nph = pb >> 4;
-          const uint8_t ph = g.nph_packed ? (uint8_t)(pb & 15) : pb;
+          const uint8_t ph = stage[Lh.phase + i];
 #pragma unroll
           for (int a = 0; a < 8; ++a) rk[q][a] = ph;
         } else {
@@ -627,7 +621,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       }
       if (MODE == kColored)
         accumulate_colored<S, 8>(acc, nd[0], c[0], nfree, valid[0], rk[0][0],
-                                 g.nph_packed ? h_nph : batch_nph(j, g.hex_bnph, h_start + b * kBatch));
+                                 batch_nph(j, g.hex_bnph, h_start + b * kBatch));
       else
         accumulate<S, 8, MODE>(acc, nd, c, nfree, valid, rk, g.max_phase_hex);
     }
@@ -739,9 +733,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   if (tid == 0 && s_bad) atomicMin(&g.flag->step, g.step_no);
 }
 
+// the step kernel instance for these arguments, with `smem` bytes of dynamic
+// shared memory allowed
 template <typename S>
-void tiled_step(const TiledArgs<S> &g, int n_parts, bool td, int mode_sel, size_t smem, cudaStream_t s) {
-  if (n_parts <= 0) return;
+void (*pick_step_kernel(const TiledArgs<S> &g, bool td, int mode_sel, size_t smem))(TiledArgs<S>) {
   using K = void (*)(TiledArgs<S>);
   // [lin][td][kinds][hex mode]; tet-only meshes ignore the hex mode.  LIN
   // only matters with temperature-dependent laws (TI never interpolates).
@@ -772,11 +767,27 @@ void tiled_step(const TiledArgs<S> &g, int n_parts, bool td, int mode_sel, size_
     FH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cfg = smem;
   }
-  kern<<<n_parts, kTileThreads, smem, s>>>(g);
+  return kern;
+}
+
+template <typename S>
+void tiled_step(const TiledArgs<S> &g, int n_parts, bool td, int mode_sel, size_t smem, cudaStream_t s) {
+  if (n_parts <= 0) return;
+  pick_step_kernel<S>(g, td, mode_sel, smem)<<<n_parts, kTileThreads, smem, s>>>(g);
   FH_CUDA(cudaGetLastError());
 }
 template void tiled_step<float>(const TiledArgs<float> &, int, bool, int, size_t, cudaStream_t);
 template void tiled_step<double>(const TiledArgs<double> &, int, bool, int, size_t, cudaStream_t);
+
+template <typename S>
+int tiled_occupancy(const TiledArgs<S> &g, bool td, int mode_sel, size_t smem) {
+  int bps = 0;
+  FH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pick_step_kernel<S>(g, td, mode_sel, smem),
+                                                        kTileThreads, smem));
+  return bps;
+}
+template int tiled_occupancy<float>(const TiledArgs<float> &, bool, int, size_t);
+template int tiled_occupancy<double>(const TiledArgs<double> &, bool, int, size_t);
 
 // ---- TI freeze ---------------------------------------------------------------
 template <typename S, int N>

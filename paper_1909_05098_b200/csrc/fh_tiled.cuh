@@ -56,7 +56,6 @@ struct TiledArgs {
   MatSet<S> mats;   // one-knot curves normalised to two knots (see normalise_curves)
   int lin;          // every curve has <= 2 knots: branch-free interpolation kernels
   int tet_rows;     // tet accumulator rows (1 or 4; tet-only meshes), see Partition::tet_rows
-  int nph_packed;   // phase bytes carry the batch's phase count in their high nibble
   int n_gauss;      // active sources, Gaussians first: src[0, n_gauss) Gaussian, [n_gauss, n_src) RF
   int n_src;
   SourceT<S> src[kMaxSources];
@@ -86,6 +85,9 @@ inline int StageBytes(int N, bool has_kf, bool has_rank, bool has_phase = false,
 
 template <typename S>
 void tiled_step(const TiledArgs<S> &g, int n_parts, bool td, int mode, size_t smem, cudaStream_t s);
+// resident step CTAs per SM of the kernel tiled_step would launch
+template <typename S>
+int tiled_occupancy(const TiledArgs<S> &g, bool td, int mode, size_t smem);
 
 // accumulation mode of the step kernel (see fh_tiled.cu): 0 ranked phases,
 // 1 corner phases, 2 corner slots (the last two need corner-unique tiles)

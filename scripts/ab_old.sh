@@ -1,5 +1,7 @@
 #!/bin/bash
-# same-box A/B: the library at an older commit (worktree _old/) vs the current one
+# Same-box A/B of the step kernel: an older commit checked out as a worktree in
+# _old/ (git worktree add _old <commit>; make -C _old/paper_1909_05098_b200/csrc)
+# against the current tree, default tile sizes, each config twice.
 mkdir -p gpurun_out/abold
 for rep in 1 2; do
   for c in cfg3 cfg5 cfg4; do

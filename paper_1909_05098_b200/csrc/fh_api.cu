@@ -1820,6 +1820,13 @@ int fh_plan_create(const fh_mesh *mesh, const fh_boundary *bnd, const fh_options
   pin.hexes = mesh->hexes;
   pin.node_class = cls.data();
   pin.target_part_nodes = opts->part_nodes > 0 ? opts->part_nodes : default_part_nodes(opts->precision, mesh->n_tets, mesh->n_hexes);
+  // the engine's default tile size, first pass (the second, occupancy-measured
+  // pass needs a GPU: pass part_nodes explicitly to pin the plan)
+  if (opts->part_nodes <= 0 && mesh->n_nodes / pin.target_part_nodes < 2 * 148)
+    pin.target_part_nodes = (int)std::max<int64_t>(96, mesh->n_nodes / (2 * 148));
+  else if (opts->part_nodes <= 0)
+    pin.target_part_nodes = wave_fit_part_nodes(pin.target_part_nodes, mesh->n_nodes, std::max(1, opts->n_domains),
+                                                opts->precision, mesh->n_tets, mesh->n_hexes, opts->device);
   pin.batch = kBatch;
   // layout tuning knobs (scripts/sweep.py): hex colour order, first-touch node order
   if (const char *env = getenv("FH_HEX_COLOR")) pin.hex_color = atoi(env);

@@ -291,8 +291,9 @@ def main():
     p_out = [C.cast(C.c_void_p(t.data_ptr()), N.f64p) for t in Touts]
     K = args.e2e_steps
     if world == 1:
-        N.check(L.fh_step_host_async(h, p_in, p_out[0], T.size, 1, dt, 0))
-        N.check(L.fh_host_wait(h, 0, C.byref(rep)))
+        for q in (0, 1):  # warm both slots (buffers, streams, events)
+            N.check(L.fh_step_host_async(h, p_in, p_out[q], T.size, 1, dt, q))
+            N.check(L.fh_host_wait(h, q, C.byref(rep)))
         t0 = time.perf_counter()
         for k in range(K):
             N.check(L.fh_step_host_async(h, p_in, p_out[k % 2], T.size, 1, dt, k % 2))

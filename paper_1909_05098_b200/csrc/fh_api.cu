@@ -1274,10 +1274,12 @@ int fh_step_host_async(fh_engine *e, const double *T_in, double *T_out, int64_t 
     FH_CUDA(cudaMallocHost(reinterpret_cast<void **>(&e->io_flag), 2 * sizeof(FailFlag)));
   }
   cudaEvent_t *ev = e->io_ev[slot];
-  if (!e->io_in[slot].p) {
-    e->io_in[slot].alloc(e->V);
-    e->io_out[slot].alloc(e->V);
-    for (int k = 0; k < 4; ++k) FH_CUDA(cudaEventRecord(ev[k], e->stream));  // all free
+  if (!e->io_in[0].p) {  // both slots at once: no allocation once the pipeline runs
+    for (int q = 0; q < 2; ++q) {
+      e->io_in[q].alloc(e->V);
+      e->io_out[q].alloc(e->V);
+      for (int k = 0; k < 4; ++k) FH_CUDA(cudaEventRecord(e->io_ev[q][k], e->stream));  // all free
+    }
   }
   // upload on its own stream once the slot's previous field was consumed
   FH_CUDA(cudaStreamWaitEvent(e->io_h2d, ev[1], 0));

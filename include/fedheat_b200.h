@@ -245,6 +245,8 @@ int fh_get_node_order(fh_engine *e, int64_t *new_to_old, int64_t n);
 /* multi-GPU: NCCL bootstrap.  Rank 0 creates the id (128 bytes), the
  * caller broadcasts it (torch.distributed), every rank attaches. */
 int fh_nccl_unique_id(char *id128);
+/* world == 1 builds a one-rank communicator (the fail-flag all-reduce then
+ * goes through NCCL): a single-GPU check of the NCCL loading and init path */
 int fh_attach_nccl(fh_engine *e, const char *id128, int32_t rank, int32_t world);
 
 /* Halo bookkeeping of a multi-domain engine (rank = domain_lo / width, world =

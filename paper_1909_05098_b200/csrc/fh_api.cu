@@ -1703,7 +1703,7 @@ int fh_attach_nccl(fh_engine *e, const char *id128, int32_t rank, int32_t world)
   if (e->assembly != FH_ASSEMBLY_TILED) fail(FH_ERR_CONFIG, "multi-GPU needs TILED mode");
   if (world != e->X.world || rank != e->X.rank)
     fail(FH_ERR_CONFIG, "rank/world do not match the engine's domain range");
-  if (world > 1 && !e->comm) {
+  if (!e->comm) {  // world 1: a one-rank communicator (only the fail-flag all-reduce uses it)
     NcclUniqueId id;
     std::memcpy(id.internal, id128, sizeof(id.internal));
     e->comm = nccl_comm_init(id, rank, world);

@@ -54,3 +54,27 @@ def test_two_ranks_match_single_engine_bitwise(prec, slab):
     for e in ranks:
         m = e.owned_mask()
         assert np.array_equal(e.temperature()[m], T[m])
+
+
+def test_nccl_one_rank_communicator():
+    """The NCCL path on one GPU: libnccl is dlopen'ed, a one-rank communicator
+    is built from fh_nccl_unique_id, and the per-call fail-flag all-reduce goes
+    through it -- the field must equal an engine without NCCL bit for bit, and
+    an unstable step must still be reported."""
+    mesh = fh.jittered_cube_mesh("hex", 10, 0.1, 0.15, seed=5)
+    mat = fh.TissueMaterial.constant(density=1060.0, specific_heat=3600.0, conductivity=0.5)
+    bnd = fh.BoundarySpec(dirichlet=(("z0", 37.0),), heat_loads=(("center", 1.0, 0.0, 1e9),))
+    kw = dict(assembly="tiled", precision=32, part_nodes=100, n_domains=8, domains=domain_range(0, 1))
+    plain = fh.ExplicitEngine(mesh, mat, bnd, **kw)
+    nccl = fh.ExplicitEngine(mesh, mat, bnd, **kw)
+    uid = C.create_string_buffer(128)
+    N.check(N.lib().fh_nccl_unique_id(uid))
+    N.check(N.lib().fh_attach_nccl(nccl._h, uid, 0, 1))
+    dt = 0.9 * plain.critical_dt(37.0)
+    a = plain.run(37.0, steps=50, dt=dt).state.temperatures
+    b = nccl.run(37.0, steps=50, dt=dt).state.temperatures
+    assert np.array_equal(a, b) and a.max() > 37.0
+    st = nccl.initial_state(37.0 + 0.01 * np.sin(np.arange(mesh.n_nodes)))
+    with pytest.raises(fh.InstabilityError):
+        for _ in range(400):
+            nccl.step(st, 10.0 * dt)

@@ -342,8 +342,8 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": E / e2e_s, "unit": "element-steps/s", "h2d_bytes_per_step": 8 * mesh.n_nodes,
                 "d2h_bytes_per_step": 8 * mesh.n_nodes},
-        # per rank: 1 fused step kernel (N=1); interior + boundary tiles + halo pack/unpack (N>1)
-        "gpu_launches": args.steps * (lay["kernels_per_step"] if world == 1 else 4),
+        # step kernel launches (one per tile kind and launch range) + halo pack / unpack (N > 1)
+        "gpu_launches": args.steps * (lay["kernels_per_step"] + (2 if world > 1 else 0)),
         "clocks": clocks,
     }
     if rank == 0:

@@ -157,6 +157,8 @@ struct TiledState {
   size_t smem = 0;
   int n_parts_local = 0;
   int n_boundary = 0;  // multi-GPU: leading entries of part_list that touch the halo
+  // tiles with tets at the head of the boundary / interior ranges (mixed meshes)
+  int n_mixed_b = 0, n_mixed_i = 0;
   int mode = 0;
 };
 
@@ -501,9 +503,22 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     for (int64_t i : e->dir_nodes) is_dir[P.new_of_old[i]] = 1;
     build_exchange(P, is_dir.data(), D, D / width, dlo / width, e->X);
   }
-  const std::vector<int32_t> &plist = e->X.part_order;  // boundary tiles first
+  std::vector<int32_t> plist = e->X.part_order;  // boundary tiles first
   st->n_parts_local = (int)plist.size();
   st->n_boundary = e->X.world > 1 ? e->X.n_boundary : 0;
+  // mixed meshes: inside each launch range the tiles holding tets come first,
+  // so the hex-only tiles can run the leaner hex-only kernel instance
+  bool split = e->n_tet > 0 && e->n_hex > 0;
+  if (const char *env = getenv("FH_KIND_SPLIT")) split = split && atoi(env) != 0;
+  st->n_mixed_b = st->n_boundary;
+  st->n_mixed_i = st->n_parts_local - st->n_boundary;
+  if (split) {
+    auto has_tet = [&](int32_t p) { return P.part_tet_count[p] > 0; };
+    auto mid_b = std::stable_partition(plist.begin(), plist.begin() + st->n_boundary, has_tet);
+    auto mid_i = std::stable_partition(plist.begin() + st->n_boundary, plist.end(), has_tet);
+    st->n_mixed_b = (int)(mid_b - plist.begin());
+    st->n_mixed_i = (int)(mid_i - (plist.begin() + st->n_boundary));
+  }
   st->part_list.upload(plist, s);
   if (e->X.world > 1) {
     e->x_send.upload(e->X.send_nodes, s);
@@ -825,18 +840,30 @@ void tiled_run(fh_engine *e, int64_t nsteps, double dt) {
       if (pass == 0) g.n_gauss = ns;
     }
     g.n_src = ns;
+    // the tiles [begin, begin + count) of part_list: the first n_mixed hold
+    // tets (mixed kernel), the rest only hexes (hex-only kernel instance)
+    auto launch = [&](int begin, int count, int n_mixed) {
+      g.part_begin = begin;
+      if (n_mixed == count) {
+        tiled_step(g, count, e->td, st.mode, st.smem, e->stream);
+        return;
+      }
+      tiled_step(g, n_mixed, e->td, st.mode, st.smem, e->stream);
+      TiledArgs<S> gh = g;
+      gh.tet_rec = nullptr;
+      gh.part_begin = begin + n_mixed;
+      tiled_step(gh, count - n_mixed, e->td, st.mode, st.smem, e->stream);
+    };
     if (e->X.world == 1) {
-      g.part_begin = 0;
-      tiled_step(g, st.n_parts_local, e->td, st.mode, st.smem, e->stream);
+      launch(0, st.n_parts_local, st.n_mixed_i);
     } else {
       // interior tiles need no halo: they run while the previous step's
       // exchange is still in flight on the comm stream
-      g.part_begin = st.n_boundary;
-      tiled_step(g, st.n_parts_local - st.n_boundary, e->td, st.mode, st.smem, e->stream);
+      launch(st.n_boundary, st.n_parts_local - st.n_boundary, st.n_mixed_i);
       if (e->halo_pending) FH_CUDA(cudaStreamWaitEvent(e->stream, e->ev_halo, 0));
       e->halo_pending = false;
+      launch(0, st.n_boundary, st.n_mixed_b);
       g.part_begin = 0;
-      tiled_step(g, st.n_boundary, e->td, st.mode, st.smem, e->stream);
       if (e->comm) {
         S *sendbuf = reinterpret_cast<S *>(e->x_sendbuf.p);
         S *recvbuf = reinterpret_cast<S *>(e->x_recvbuf.p);
@@ -1519,7 +1546,12 @@ int fh_get_layout(fh_engine *e, fh_layout *out) {
                       e->V * 8 * 8;
   } else {
     const Partition &P = e->part;
-    out->kernels_per_step = 1;
+    auto launches = [&](const auto &st) {  // one per tile kind present in each launch range
+      const int ni = st.n_parts_local - st.n_boundary;
+      return (st.n_mixed_i > 0 && st.n_mixed_i < ni ? 2 : 1) +
+             (st.n_boundary ? (st.n_mixed_b > 0 && st.n_mixed_b < st.n_boundary ? 2 : 1) : 0);
+    };
+    out->kernels_per_step = e->precision == 32 ? launches(*e->tf) : launches(*e->tdd);
     out->n_parts = P.n_parts;
     out->max_part_nodes = P.max_part_nodes;
     const int64_t nts = (int64_t)P.tet_slot_elem.size(), nhs = (int64_t)P.hex_slot_elem.size();

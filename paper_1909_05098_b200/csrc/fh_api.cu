@@ -150,7 +150,7 @@ struct TiledState {
   DBuf<int32_t> tet_conn, hex_conn, tet_slot_elem, hex_slot_elem;
   DBuf<S> tet_kf, hex_kf, tet_kbar, hex_kbar;
   DBuf<uint8_t> tet_rank, hex_rank, tet_region, hex_region, node_region;
-  DBuf<int8_t> part_mat;
+  DBuf<int8_t> part_mat, part_region;
   DBuf<uint8_t> tet_phase, hex_phase, tet_bnph, hex_bnph;
   DBuf<S> T[2], vol, cap, kb, q_ext, xyz, robin_hA, robin_hAT;
   int cur = 0;
@@ -599,6 +599,23 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   if (regions) {
     st->tet_region.alloc(nts);
     st->hex_region.alloc(nhs);
+    // tiles whose slots all lie in one region skip the per-slot region bytes
+    std::vector<int8_t> pr(P.n_parts);
+    for (int p = 0; p < P.n_parts; ++p) {
+      int r = -2;
+      auto scan = [&](const std::vector<int32_t> &slot_elem, int32_t start, int32_t count) {
+        for (int32_t q = start; q < start + count && r != -1; ++q) {
+          const int32_t el = slot_elem[q];
+          if (el < 0) continue;
+          const int re = o.element_region[el];
+          r = (r == -2 || r == re) ? re : -1;
+        }
+      };
+      scan(P.tet_slot_elem, P.part_tet_start[p], P.part_tet_count[p]);
+      scan(P.hex_slot_elem, P.part_hex_start[p], P.part_hex_count[p]);
+      pr[p] = (int8_t)(r < 0 || r > 127 ? -1 : r);
+    }
+    st->part_region.upload(pr, s);
   }
   if (nts)
     k_pack_slots<S><<<nblk(nts), kBlk, 0, s>>>(st->tet_slot_elem.p, nts, G_dev, 1.0,
@@ -707,6 +724,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.xyzv = st->xyz.p;
   g.node_region = st->node_region.p;
   g.part_mat = st->part_mat.p;
+  g.part_region = st->part_region.p;
   g.robin_hA = st->robin_hA.p;
   g.robin_hAT = st->robin_hAT.p;
   g.mats = mats_of<S>(e);

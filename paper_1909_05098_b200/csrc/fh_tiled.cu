@@ -196,14 +196,15 @@ __device__ __forceinline__ S sources_at(const TiledArgs<S> &g, const S *xyz) {
     const SourceT<S> &s = g.src[k];
     const S dx = x - s.cx, dy = y - s.cy, dz = z - s.cz;
     const S r2 = (dx * dx + dy * dy) + dz * dz;
-    q += r2 > S(0) ? min(s.cap, s.inv4pi_amp / r2) : s.cap;
+    q += r2 > S(0) ? min(s.cap, fast_div(s.inv4pi_amp, r2)) : s.cap;
   }
   return q;
 }
 
 // Issue the bulk copies of batch j of part p into stage buffer `st`.
 template <typename S>
-__device__ void issue_batch(const TiledArgs<S> &g, int p, int j, int nbt, unsigned char *stage, uint64_t *bar) {
+__device__ void issue_batch(const TiledArgs<S> &g, int p, int j, int nbt, unsigned char *stage, uint64_t *bar,
+                            bool with_region = true) {
   const bool tet = j < nbt;
   const int N = tet ? 4 : 8;
   const int b = tet ? j : j - nbt;
@@ -215,8 +216,9 @@ __device__ void issue_batch(const TiledArgs<S> &g, int p, int j, int nbt, unsign
   const S *kf = tet ? g.tet_kf : g.hex_kf;
   const uint8_t *rank = tet ? g.tet_rank : g.hex_rank;
   const uint8_t *phase = tet ? g.tet_phase : g.hex_phase;
-  const uint8_t *region = tet ? g.tet_region : g.hex_region;
-  const StageLayout<S> L(N, kf != nullptr, rank != nullptr, region != nullptr);
+  const uint8_t *region_s = tet ? g.tet_region : g.hex_region;
+  const StageLayout<S> L(N, kf != nullptr, rank != nullptr, region_s != nullptr);
+  const uint8_t *region = with_region ? region_s : nullptr;  // uniform tiles: nothing to stage
   const int kp = (k + 15) & ~15;  // bulk copies move multiples of 16 bytes
   uint32_t bytes = (uint32_t)(kr * N * 2 + 6 * kr * sizeof(S));
   if (kf) bytes += kr * sizeof(S);
@@ -464,6 +466,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   const int t_cnt = __ldg(g.part_tet_count + p), h_cnt = __ldg(g.part_hex_count + p);
   const int t_start = __ldg(g.part_tet_start + p), h_start = __ldg(g.part_hex_start + p);
   const int nbt = (t_cnt + kBatch - 1) / kBatch;
+  // several materials: the tile's slots may all share one region (then no
+  // region bytes are staged and every slot uses it), else -1
+  const int preg = g.part_region ? (int)g.part_region[p] : -1;
   const int nbh = (g.part_hex_count[p] + kBatch - 1) / kBatch;
   const int nb = nbt + nbh;
   // the tile's halo id list is bulk-copied into the (not yet used) accumulator
@@ -490,7 +495,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
     const uint32_t hbytes = (uint32_t)((((h0 + nh + 3) & ~3) - hs) * 4);
     mbar_expect_tx(&hbar, hbytes);
     if (hbytes) bulk_g2s(s_ids, g.halo_nodes + hs, hbytes, &hbar);
-    for (int j = 0; j < kStages && j < nb; ++j) issue_batch(g, p, j, nbt, ring + j * g.stage_bytes, &bars[j]);
+    for (int j = 0; j < kStages && j < nb; ++j)
+      issue_batch(g, p, j, nbt, ring + j * g.stage_bytes, &bars[j], preg < 0);
 #if FH_PREFETCH_NODES
     // the node update's per-node streams, pulled into L2 while the batches run
     if (g.n_src) prefetch_range(g.xyzv + 4 * (size_t)n0, 4 * sizeof(S) * nfree);
@@ -547,11 +553,15 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
 
   // uniform per launch: stage layouts and which optional streams exist
   const bool t_kf = g.tet_kf != nullptr, h_kf = g.hex_kf != nullptr;
-  const bool t_reg = g.tet_region != nullptr, h_reg = g.hex_region != nullptr;
+  // stage layouts follow the global streams; t_reg / h_reg: this tile reads
+  // its slots' region bytes (otherwise they all use tile_reg)
+  const bool t_rs = g.tet_region != nullptr, h_rs = g.hex_region != nullptr;
+  const bool t_reg = t_rs && preg < 0, h_reg = h_rs && preg < 0;
+  const int tile_reg = preg < 0 ? 0 : preg;
   const bool t_col = g.tet_phase != nullptr;
   const uint32_t t_mask = g.tet_rows > 1 ? 0x3fffu : 0xffffu;  // row-tagged tet connectivity
-  const StageLayout<S> Lt(4, t_kf, !t_col, t_reg);
-  const StageLayout<S> Lh(8, h_kf, MODE == kRanked, h_reg);
+  const StageLayout<S> Lt(4, t_kf, !t_col, t_rs);
+  const StageLayout<S> Lh(8, h_kf, MODE == kRanked, h_rs);
   auto batch_nph = [&](int jj, const uint8_t *bn, int slot0) -> int {
     return jj < kNphCache ? (int)s_nph[jj] : (int)__ldg(bn + slot0 / kBatch);
   };
@@ -576,7 +586,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         // slots past the end of a partial batch read slot 0 (always present)
         // instead of branching; only their accumulation is predicated off
         const int i = valid[q] ? q * kTileThreads + tid : 0;
-        const int reg = t_reg ? (int)stage[Lt.region + i] : 0;
+        const int reg = t_reg ? (int)stage[Lt.region + i] : tile_reg;
         tet_loads<S, TD, LIN>(g, stage, sT, reg, t_kf, i, nd[q], c[q], rofs[q], t_mask, nfree);
         // tets are never corner-unique: colour phases (phase byte per slot) or,
         // if the colouring overflowed, ranked phases (rank byte per corner)
@@ -601,7 +611,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
 #pragma unroll
       for (int q = 0; q < kSPT; ++q) {
         const int i = valid[q] ? q * kTileThreads + tid : 0;
-        const int reg = h_reg ? (int)stage[Lh.region + i] : 0;
+        const int reg = h_reg ? (int)stage[Lh.region + i] : tile_reg;
         hex_loads<S, TD, LIN>(g, stage, sT, reg, h_kf, i, nd[q], c[q]);
         if (MODE == kRanked) {
           const uint2 w = reinterpret_cast<const uint2 *>(stage + Lh.rank)[i];
@@ -628,7 +638,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
     // every thread passed the last phase barrier: the stage can be refilled
     if (tid == 0 && j + kStages < nb) {
       fence_proxy_async();
-      issue_batch(g, p, j + kStages, nbt, stage, &bars[st]);
+      issue_batch(g, p, j + kStages, nbt, stage, &bars[st], preg < 0);
     }
     if (++st == kStages) {
       st = 0;
@@ -702,7 +712,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
           const SourceT<S> &sr = g.src[0];
           const S dx = px[u] - sr.cx, dy = py[u] - sr.cy, dz = pz[u] - sr.cz;
           const S r2 = (dx * dx + dy * dy) + dz * dz;
-          rate += (r2 > S(0) ? min(sr.cap, sr.inv4pi_amp / r2) : sr.cap) * v[u];
+          rate += (r2 > S(0) ? min(sr.cap, fast_div(sr.inv4pi_amp, r2)) : sr.cap) * v[u];
         } else if (KIND == 0 && g.n_src) {
           const S xyz[3] = {px[u], py[u], pz[u]};
           rate += sources_at(g, xyz) * v[u];

@@ -52,6 +52,7 @@ struct TiledArgs {
   const S *xyzv;                    // (x, y, z, v) per node, for time-dependent sources
   const uint8_t *node_region;
   const int8_t *part_mat;  // with node_region: the tile's single material, or -1
+  const int8_t *part_region;  // with slot regions: the region all the tile's slots share, or -1
   const S *robin_hA, *robin_hAT;
   MatSet<S> mats;   // one-knot curves normalised to two knots (see normalise_curves)
   int lin;          // every curve has <= 2 knots: branch-free interpolation kernels

@@ -226,9 +226,14 @@ struct fh_engine {
   bool io_used[2] = {false, false};
   FailFlag *io_flag = nullptr;  // pinned: the fail flag after each slot's steps
   int refit_per_sm = 0;          // wave fit: measured resident step CTAs per SM (second pass)
+  cudaStream_t kind_stream = nullptr;  // mixed meshes: the mixed-tile launch runs beside the hex-only one
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   ~fh_engine() {
     if (io_flag) cudaFreeHost(io_flag);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (kind_stream) cudaStreamDestroy(kind_stream);
     for (auto &evs : io_ev)
       for (cudaEvent_t ev : evs)
         if (ev) cudaEventDestroy(ev);
@@ -866,11 +871,22 @@ void tiled_run(fh_engine *e, int64_t nsteps, double dt) {
         tiled_step(g, count, e->td, st.mode, st.smem, e->stream);
         return;
       }
-      tiled_step(g, n_mixed, e->td, st.mode, st.smem, e->stream);
+      // the two instances run concurrently (disjoint tiles): the mixed tiles
+      // on a side stream, so their last wave overlaps the hex-only tiles
+      if (!e->kind_stream) {
+        FH_CUDA(cudaStreamCreateWithFlags(&e->kind_stream, cudaStreamNonBlocking));
+        FH_CUDA(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
+        FH_CUDA(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
+      }
+      FH_CUDA(cudaEventRecord(e->ev_fork, e->stream));
+      FH_CUDA(cudaStreamWaitEvent(e->kind_stream, e->ev_fork, 0));
+      tiled_step(g, n_mixed, e->td, st.mode, st.smem, e->kind_stream);
+      FH_CUDA(cudaEventRecord(e->ev_join, e->kind_stream));
       TiledArgs<S> gh = g;
       gh.tet_rec = nullptr;
       gh.part_begin = begin + n_mixed;
       tiled_step(gh, count - n_mixed, e->td, st.mode, st.smem, e->stream);
+      FH_CUDA(cudaStreamWaitEvent(e->stream, e->ev_join, 0));
     };
     if (e->X.world == 1) {
       launch(0, st.n_parts_local, st.n_mixed_i);

@@ -167,7 +167,11 @@ int fh_destroy(fh_engine *e);
 /* state (original node numbering, float64 on the host side) */
 int fh_set_temperature(fh_engine *e, const double *T, int64_t n, int64_t step_index, double time);
 int fh_get_temperature(fh_engine *e, double *T, int64_t n);
-int fh_get_inflow(fh_engine *e, double *F, int64_t n); /* EXACT: last step's F */
+/* last step's net conduction inflow F (solver.py:352 state.inflow).  EXACT:
+ * always kept.  TILED: only after fh_keep_inflow(e, 1); entries of Dirichlet
+ * nodes (never updated) are 0. */
+int fh_get_inflow(fh_engine *e, double *F, int64_t n);
+int fh_keep_inflow(fh_engine *e, int32_t on);
 int fh_reset_properties(fh_engine *e);                 /* next step refreshes (TI re-freeze) */
 
 /* advance nsteps explicit steps of size dt (solver.py:348-382 each).  If

@@ -84,7 +84,7 @@ class FhLayout(C.Structure):
 EXPORTS = [
     "fh_last_error", "fh_version", "fh_device_count", "fh_eval_curve_nodes", "fh_lumped_capacity_nodes",
     "fh_element_mean_nodal", "fh_scatter_net_loads", "fh_nodal_update", "fh_create", "fh_destroy",
-    "fh_set_temperature", "fh_get_temperature", "fh_get_inflow", "fh_reset_properties", "fh_step",
+    "fh_set_temperature", "fh_get_temperature", "fh_get_inflow", "fh_keep_inflow", "fh_reset_properties", "fh_step",
     "fh_step_timed", "fh_step_timed_flush", "fh_step_host", "fh_step_host_async", "fh_host_wait", "fh_set_q_static", "fh_set_sources", "fh_set_probes", "fh_get_probes", "fh_critical_dt", "fh_scatter_loads",
     "fh_get_precompute", "fh_get_layout", "fh_stream", "fh_get_node_order", "fh_nccl_unique_id",
     "fh_attach_nccl", "fh_halo_info", "fh_halo_lists", "fh_halo_export", "fh_halo_import", "fh_get_owned",
@@ -113,6 +113,7 @@ def lib():
     L.fh_set_temperature.argtypes = [C.c_void_p, f64p, C.c_int64, C.c_int64, C.c_double]
     L.fh_get_temperature.argtypes = [C.c_void_p, f64p, C.c_int64]
     L.fh_get_inflow.argtypes = [C.c_void_p, f64p, C.c_int64]
+    L.fh_keep_inflow.argtypes = [C.c_void_p, C.c_int32]
     L.fh_reset_properties.argtypes = [C.c_void_p]
     L.fh_step.argtypes = [C.c_void_p, C.c_int64, C.c_double, C.POINTER(FhReport)]
     L.fh_step_timed.argtypes = [C.c_void_p, C.c_int64, C.c_double, C.POINTER(FhReport), C.POINTER(C.c_float)]

@@ -98,6 +98,21 @@ __global__ void k_to_new(const double *__restrict__ src_old, const int64_t *__re
   if (dd2) dd2[n] = v;
 }
 
+// TILED: Dirichlet values written into both temperature buffers (new numbering);
+// the step kernel never updates these nodes, so they hold the values exactly
+template <typename S>
+__global__ void k_scatter_dir(S *__restrict__ T0, S *__restrict__ T1, const int32_t *__restrict__ ids,
+                              const S *__restrict__ vals, int64_t n) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  T0[ids[q]] = vals[q];
+  T1[ids[q]] = vals[q];
+}
+
+// a Dirichlet value beyond the runaway limit fails every step (the reference
+// checks max |T| over all nodes after the overwrite, solver.py:369-370)
+__global__ void k_flag_step(FailFlag *flag, unsigned long long step_no) { atomicMin(&flag->step, step_no); }
+
 template <typename S>
 __global__ void k_to_old(const S *__restrict__ src_new, const int64_t *__restrict__ new_of_old, int64_t V,
                          double *__restrict__ dst_old) {
@@ -153,6 +168,8 @@ struct TiledState {
   DBuf<int8_t> part_mat, part_region;
   DBuf<uint8_t> tet_phase, hex_phase, tet_bnph, hex_bnph;
   DBuf<S> T[2], vol, cap, kb, q_ext, xyz, robin_hA, robin_hAT;
+  DBuf<int32_t> dir_ids;  // Dirichlet nodes (new numbering) and their values
+  DBuf<S> dir_vals, F;    // F: net conduction inflow of the updated nodes (ExplicitEngine.step)
   int cur = 0;
   size_t smem = 0;
   int n_parts_local = 0;
@@ -171,6 +188,10 @@ struct fh_engine {
   bool td = false;
   int64_t V = 0, E = 0, n_tet = 0, n_hex = 0, nconn = 0;
   double runaway_limit = 1e6;
+  bool dir_runaway = false;  // some |Dirichlet value| > runaway_limit: every step fails
+  bool keep_inflow = false;  // TILED: the step kernel also writes F (fh_keep_inflow)
+  bool io_failed = false;    // an async step failed: fh_set_temperature must come first
+  double io_dt = 0.0;        // dt of the last fh_step_host_async (clock rollback on failure)
   int64_t step_index = 0;
   double time = 0.0;
   bool frozen = false;
@@ -716,6 +737,16 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     st->robin_hA.upload(ha, s);
     st->robin_hAT.upload(hat, s);
   }
+  if (!e->dir_nodes.empty()) {  // imposed on the device whenever a field is set (solver.py:364-365)
+    std::vector<int32_t> ids(e->dir_nodes.size());
+    std::vector<S> vals(e->dir_nodes.size());
+    for (size_t q = 0; q < e->dir_nodes.size(); ++q) {
+      ids[q] = (int32_t)P.new_of_old[e->dir_nodes[q]];
+      vals[q] = (S)e->dir_vals[q];
+    }
+    st->dir_ids.upload(ids, s);
+    st->dir_vals.upload(vals, s);
+  }
   g.part_list = st->part_list.p;
   g.part_node_start = st->part_node_start.p;
   g.part_n_free = st->part_n_free.p;
@@ -819,6 +850,9 @@ void tiled_set_T(fh_engine *e, const double *src = nullptr) {  // src (default e
     d1 = st.T[1].p;
   }
   k_to_new<<<nblk(e->V), kBlk, 0, e->stream>>>(src ? src : e->stage.p, e->old_of_new.p, e->V, f0, d0, f1, d1);
+  if (st.dir_ids.n)
+    k_scatter_dir<S><<<nblk((int64_t)st.dir_ids.n), kBlk, 0, e->stream>>>(st.T[0].p, st.T[1].p, st.dir_ids.p,
+                                                                         st.dir_vals.p, (int64_t)st.dir_ids.n);
   FH_CUDA(cudaGetLastError());
   st.cur = 0;
 }
@@ -862,6 +896,7 @@ void tiled_run(fh_engine *e, int64_t nsteps, double dt) {
     }
     g.dt = (S)dt;
     g.step_no = (unsigned long long)(e->step_index + 1);
+    g.F_out = e->keep_inflow ? st.F.p : nullptr;
     // active sources only, Gaussians first (the kernel loops over each kind
     // without per-source branches)
     int ns = 0;
@@ -930,6 +965,7 @@ void tiled_run(fh_engine *e, int64_t nsteps, double dt) {
         e->halo_pending = true;
       }
     }
+    if (e->dir_runaway) k_flag_step<<<1, 1, 0, e->stream>>>(e->flag.p, g.step_no);
     st.cur ^= 1;
     e->step_index += 1;
     e->time = (double)e->step_index * dt;
@@ -952,6 +988,7 @@ void exact_run(fh_engine *e, int64_t nsteps, double dt) {
       e->frozen = true;
     }
     exact_step(e->ex, e->T.p, dt, t, e->step_index + 1, e->td, e->stream);
+    if (e->dir_runaway) k_flag_step<<<1, 1, 0, e->stream>>>(e->flag.p, (unsigned long long)(e->step_index + 1));
     e->step_index += 1;
     e->time = (double)e->step_index * dt;
     if (e->n_probes && e->step_index % e->probe_interval == 0 && e->n_rec < e->probe_cap) {
@@ -1130,6 +1167,8 @@ int fh_create(const fh_mesh *mesh, const fh_boundary *bnd, const fh_options *opt
   e->dir_vals.assign(bnd->dirichlet_values, bnd->dirichlet_values + bnd->n_dirichlet);
   for (int64_t i : e->dir_nodes)
     if (i < 0 || i >= e->V) fail(FH_ERR_CONFIG, "Dirichlet node out of range");
+  for (double v : e->dir_vals)
+    if (!(std::fabs(v) <= e->runaway_limit)) e->dir_runaway = true;
   if (bnd->n_loads > 0) {
     e->load_offs.assign(bnd->load_offsets, bnd->load_offsets + bnd->n_loads + 1);
     e->load_nodes.assign(bnd->load_nodes, bnd->load_nodes + e->load_offs.back());
@@ -1272,6 +1311,7 @@ int fh_set_temperature(fh_engine *e, const double *T, int64_t n, int64_t step_in
     tiled_set_T<double>(e);
   e->step_index = step_index;
   e->time = time;
+  e->io_failed = false;
   FH_CUDA(cudaStreamSynchronize(e->stream));
   FH_API_END
 }
@@ -1289,10 +1329,38 @@ int fh_get_temperature(fh_engine *e, double *T, int64_t n) {
 int fh_get_inflow(fh_engine *e, double *F, int64_t n) {
   FH_API_BEGIN
   check_engine(e);
-  if (e->assembly != FH_ASSEMBLY_EXACT) fail(FH_ERR_CONFIG, "inflow is only kept in EXACT mode");
   if (n != e->V) fail(FH_ERR_CONFIG, "output has the wrong length");
-  FH_CUDA(cudaMemcpyAsync(F, e->F.p, sizeof(double) * e->V, cudaMemcpyDeviceToHost, e->stream));
+  if (e->assembly == FH_ASSEMBLY_EXACT) {
+    FH_CUDA(cudaMemcpyAsync(F, e->F.p, sizeof(double) * e->V, cudaMemcpyDeviceToHost, e->stream));
+  } else {
+    if (!e->keep_inflow) fail(FH_ERR_CONFIG, "TILED mode keeps the inflow only after fh_keep_inflow(e, 1)");
+    auto get = [&](auto &st) {
+      using S = std::remove_reference_t<decltype(*st.T[0].p)>;
+      k_to_old<S><<<nblk(e->V), kBlk, 0, e->stream>>>(st.F.p, e->new_of_old.p, e->V, e->stage.p);
+      FH_CUDA(cudaGetLastError());
+    };
+    if (e->precision == 32) get(*e->tf); else get(*e->tdd);
+    FH_CUDA(cudaMemcpyAsync(F, e->stage.p, sizeof(double) * e->V, cudaMemcpyDeviceToHost, e->stream));
+  }
   FH_CUDA(cudaStreamSynchronize(e->stream));
+  FH_API_END
+}
+
+int fh_keep_inflow(fh_engine *e, int32_t on) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (e->assembly == FH_ASSEMBLY_EXACT) return FH_OK;  // EXACT always keeps F
+  e->keep_inflow = on != 0;
+  if (e->keep_inflow) {
+    auto alloc = [&](auto &st) {
+      if (!st.F.p) {
+        st.F.alloc(e->V);
+        st.F.zero(e->stream);  // Dirichlet nodes are not updated: their entries stay 0
+        FH_CUDA(cudaStreamSynchronize(e->stream));
+      }
+    };
+    if (e->precision == 32) alloc(*e->tf); else alloc(*e->tdd);
+  }
   FH_API_END
 }
 
@@ -1346,6 +1414,8 @@ int fh_step_host_async(fh_engine *e, const double *T_in, double *T_out, int64_t 
   if (nsteps < 0) fail(FH_ERR_CONFIG, "nsteps must be >= 0");
   if (!(dt > 0.0) || !std::isfinite(dt)) fail(FH_ERR_CONFIG, "dt must be positive and finite");
   if (e->io_used[slot]) fail(FH_ERR_CONFIG, "slot still in flight: call fh_host_wait first");
+  if (e->io_failed) fail(FH_ERR_CONFIG, "an asynchronous step failed: call fh_set_temperature first");
+  e->io_dt = dt;
   if (!e->io_h2d) {
     FH_CUDA(cudaStreamCreateWithFlags(&e->io_h2d, cudaStreamNonBlocking));
     FH_CUDA(cudaStreamCreateWithFlags(&e->io_d2h, cudaStreamNonBlocking));
@@ -1403,7 +1473,21 @@ int fh_host_wait(fh_engine *e, int32_t slot, fh_report *rep) {
     rep->step_index = e->step_index;
   }
   if (f.step != ~0ull) {
-    if (rep) rep->fail_step = (int64_t)f.step;
+    // the engine stops here: later queued steps were no-ops; the clock goes
+    // back to the failing step, the flag is cleared and further async calls
+    // are refused until a field is set again (fh_set_temperature)
+    FH_CUDA(cudaStreamSynchronize(e->stream));
+    const FailFlag clear{~0ull};
+    FH_CUDA(cudaMemcpyAsync(e->flag.p, &clear, sizeof(clear), cudaMemcpyHostToDevice, e->stream));
+    FH_CUDA(cudaStreamSynchronize(e->stream));
+    e->step_index = (int64_t)f.step;
+    e->time = (double)f.step * e->io_dt;
+    e->io_failed = true;
+    if (rep) {
+      rep->fail_step = (int64_t)f.step;
+      rep->time = e->time;
+      rep->step_index = e->step_index;
+    }
     fail(FH_ERR_INSTABILITY, "step " + std::to_string((int64_t)f.step) +
                                  ": non-finite or runaway temperature (fh_step_host_async)");
   }

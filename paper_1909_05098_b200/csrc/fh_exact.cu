@@ -65,8 +65,9 @@ __global__ void k_exact_props(ExactArgs g, const double *__restrict__ T) {
 }
 
 __global__ void k_exact_elem(ExactArgs g, const double *__restrict__ T, int use_frozen_kbar,
-                             const double *__restrict__ kbar_in) {
-  if (g.flag && g.flag->step != kNoFail) return;
+                             const double *__restrict__ kbar_in, unsigned long long step_no) {
+  // skip only when an earlier step failed (the failing step runs to completion)
+  if (g.flag && g.flag->step < step_no) return;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= g.E) return;
   const double ke = kbar_in ? kbar_in[e] : (use_frozen_kbar ? g.kbar[e] : elem_kbar(g, e, T));
@@ -113,7 +114,7 @@ __device__ double source_density(const fh_source &s, double x, double y, double 
 
 __global__ void k_exact_node(ExactArgs g, double *__restrict__ T, double dt, double t_start,
                              unsigned long long step_no, int td) {
-  if (g.flag && g.flag->step != kNoFail) return;
+  if (g.flag && g.flag->step < step_no) return;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   bool bad = false;
   if (i < g.V) {
@@ -175,7 +176,8 @@ void exact_props(const ExactArgs &g, const double *T, cudaStream_t s) {
 
 void exact_step(const ExactArgs &g, double *T, double dt, double t_start, int64_t step_no, bool td,
                 cudaStream_t s) {
-  k_exact_elem<<<(unsigned)((g.E + 255) / 256), 256, 0, s>>>(g, T, td ? 0 : 1, nullptr);
+  k_exact_elem<<<(unsigned)((g.E + 255) / 256), 256, 0, s>>>(g, T, td ? 0 : 1, nullptr,
+                                                              (unsigned long long)step_no);
   k_exact_node<<<(unsigned)((g.V + 255) / 256), 256, 0, s>>>(g, T, dt, t_start, (unsigned long long)step_no,
                                                               td ? 1 : 0);
   FH_CUDA(cudaGetLastError());
@@ -190,7 +192,7 @@ __global__ void k_exact_gather_only(ExactArgs g, double *__restrict__ out) {
 void exact_scatter(const ExactArgs &g, const double *kbar, const double *T, double *out, cudaStream_t s) {
   ExactArgs h = g;
   h.flag = nullptr;
-  k_exact_elem<<<(unsigned)((g.E + 255) / 256), 256, 0, s>>>(h, T, 0, kbar);
+  k_exact_elem<<<(unsigned)((g.E + 255) / 256), 256, 0, s>>>(h, T, 0, kbar, 0ull);
   k_exact_gather_only<<<(unsigned)((g.V + 255) / 256), 256, 0, s>>>(h, out);
   FH_CUDA(cudaGetLastError());
 }

@@ -456,7 +456,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   // phases per batch of the tile (colour modes), read once instead of per batch
   constexpr int kNphCache = 64;
   __shared__ uint8_t s_nph[kNphCache];
-  if (g.flag->step != kNone) return;
+  // skip only when an EARLIER step failed: every CTA of the failing step still
+  // writes its tile, so the field after a runaway is that whole step's output
+  if (g.flag->step < g.step_no) return;
   const int p = g.part_list ? g.part_list[g.part_begin + blockIdx.x] : g.part_begin + (int)blockIdx.x;
   const int tid = threadIdx.x;
   const int n0 = g.part_node_start[p];
@@ -723,6 +725,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         }
         const S xn = x + fast_div(g.dt * rate, cap);
         if (ok) {
+          if (g.F_out) g.F_out[n] = Fsum;
           g.Tout[n] = xn;
           bad |= !(fabs(xn) <= g.runaway_limit);  // also catches NaN
         }

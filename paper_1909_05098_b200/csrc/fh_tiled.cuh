@@ -46,6 +46,7 @@ struct TiledArgs {
   // nodes (new numbering)
   const S *Tin;
   S *Tout;
+  S *F_out;  // optional: net conduction inflow of the updated nodes (ExplicitEngine.step's state.inflow)
   const S *vol;
   const S *cap_frozen, *kb_frozen;  // TI
   const S *q_ext;                   // heat loads + static sources (W) or null

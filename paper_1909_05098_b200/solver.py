@@ -312,6 +312,7 @@ class ExplicitEngine:
         self.assembly = assembly
         self.sources = tuple(sources)
         self._packed = None
+        self._inflow_kept = False
         N.require_gpu()
         fm, fb, fo, keep, self.robin = native_inputs(
             mesh, self.boundary, self.materials, sources=self.sources, robin=robin, kfactor=kfactor,
@@ -440,13 +441,17 @@ class ExplicitEngine:
         T = state.temperatures
         if T.dtype != np.float64 or not T.flags.c_contiguous:
             raise ConfigError("state.temperatures must be a contiguous float64 array")
+        # one upload (fh_set_temperature: field + clock), the step, one download
         N.check(self._L.fh_set_temperature(self._h, N.ptr(T), T.size, int(state.step_index), float(state.time)))
+        if self.assembly != "exact" and not self._inflow_kept:
+            N.check(self._L.fh_keep_inflow(self._h, 1))  # TILED: the step kernel also writes F
+            self._inflow_kept = True
         rep = N.FhReport()
         rc = self._L.fh_step_host(self._h, None, N.ptr(T), T.size, 1, float(dt), C.byref(rep))
         state.step_index = int(rep.step_index)
         state.time = float(rep.time)
-        if self.assembly == "exact":
-            N.check(self._L.fh_get_inflow(self._h, N.ptr(state.inflow), T.size))
+        # state.inflow = this step's F (solver.py:352); TILED: 0 at Dirichlet nodes
+        N.check(self._L.fh_get_inflow(self._h, N.ptr(state.inflow), T.size))
         if rc == 2:
             self._raise_instability(state, rep)
         N.check(rc)
@@ -531,7 +536,7 @@ class ExplicitEngine:
         N.check(self._L.fh_get_temperature(self._h, N.ptr(T), T.size))
         stepping = _time.perf_counter() - t_begin
         state.step_index, state.time = done, float(rep.time)
-        if self.assembly == "exact":
+        if self.assembly == "exact" or self._inflow_kept:
             N.check(self._L.fh_get_inflow(self._h, N.ptr(state.inflow), T.size))
         if on_snapshot is not None:
             on_snapshot(state)

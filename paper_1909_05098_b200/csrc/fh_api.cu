@@ -98,15 +98,12 @@ __global__ void k_to_new(const double *__restrict__ src_old, const int64_t *__re
   if (dd2) dd2[n] = v;
 }
 
-// TILED: Dirichlet values written into both temperature buffers (new numbering);
-// the step kernel never updates these nodes, so they hold the values exactly
+// TILED: Dirichlet values written into a temperature buffer (new numbering);
+// the step kernel never updates these nodes, so they keep the values exactly
 template <typename S>
-__global__ void k_scatter_dir(S *__restrict__ T0, S *__restrict__ T1, const int32_t *__restrict__ ids,
-                              const S *__restrict__ vals, int64_t n) {
+__global__ void k_scatter_dir(S *T, const int32_t *__restrict__ ids, const S *__restrict__ vals, int64_t n) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= n) return;
-  T0[ids[q]] = vals[q];
-  T1[ids[q]] = vals[q];
+  if (q < n) T[ids[q]] = vals[q];
 }
 
 // a Dirichlet value beyond the runaway limit fails every step (the reference
@@ -170,6 +167,7 @@ struct TiledState {
   DBuf<S> T[2], vol, cap, kb, q_ext, xyz, robin_hA, robin_hAT;
   DBuf<int32_t> dir_ids;  // Dirichlet nodes (new numbering) and their values
   DBuf<S> dir_vals, F;    // F: net conduction inflow of the updated nodes (ExplicitEngine.step)
+  bool dir_pending = false;  // T[cur] (the field as set) still lacks the Dirichlet values
   int cur = 0;
   size_t smem = 0;
   int n_parts_local = 0;
@@ -850,9 +848,14 @@ void tiled_set_T(fh_engine *e, const double *src = nullptr) {  // src (default e
     d1 = st.T[1].p;
   }
   k_to_new<<<nblk(e->V), kBlk, 0, e->stream>>>(src ? src : e->stage.p, e->old_of_new.p, e->V, f0, d0, f1, d1);
+  // the reference steps from the state as given and imposes the Dirichlet
+  // values after the update (solver.py:364-365): the first step reads T[0]
+  // as set and writes T[1], which already holds the Dirichlet values (the
+  // kernel never writes those nodes); T[0] gets them right after that step
   if (st.dir_ids.n)
-    k_scatter_dir<S><<<nblk((int64_t)st.dir_ids.n), kBlk, 0, e->stream>>>(st.T[0].p, st.T[1].p, st.dir_ids.p,
+    k_scatter_dir<S><<<nblk((int64_t)st.dir_ids.n), kBlk, 0, e->stream>>>(st.T[1].p, st.dir_ids.p,
                                                                          st.dir_vals.p, (int64_t)st.dir_ids.n);
+  st.dir_pending = st.dir_ids.n > 0;
   FH_CUDA(cudaGetLastError());
   st.cur = 0;
 }
@@ -966,6 +969,12 @@ void tiled_run(fh_engine *e, int64_t nsteps, double dt) {
       }
     }
     if (e->dir_runaway) k_flag_step<<<1, 1, 0, e->stream>>>(e->flag.p, g.step_no);
+    if (st.dir_pending) {  // this step's input buffer is the next step's output
+      k_scatter_dir<S><<<nblk((int64_t)st.dir_ids.n), kBlk, 0, e->stream>>>(
+          st.T[st.cur].p, st.dir_ids.p, st.dir_vals.p, (int64_t)st.dir_ids.n);
+      FH_CUDA(cudaGetLastError());
+      st.dir_pending = false;
+    }
     st.cur ^= 1;
     e->step_index += 1;
     e->time = (double)e->step_index * dt;

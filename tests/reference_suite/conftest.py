@@ -26,6 +26,7 @@ the reason listed in SKIPS.
 
 from __future__ import annotations
 
+import importlib
 import importlib.util
 import os
 import sys
@@ -60,14 +61,9 @@ def _install_aliases() -> bool:
     from paper_1909_05098_b200 import (element, errors, kernels, material, mesh, meshgen, meshio, precompute,
                                        solver, vtkio)
 
-    pkg = types.ModuleType("fedheat")
-    pkg.__path__ = [REF_PKG]  # modules not aliased below load from the reference package
-    pkg.__fh_alias__ = True
-    pkg.__dict__.update({k: getattr(fh, k) for k in fh.__all__})
-    pkg.kernels = kernels
-    sys.modules["fedheat"] = pkg
-    # fedheat.mesh = the facade's Mesh + its text parser / writer (meshio.py)
-    mesh_mod = types.ModuleType("fedheat.mesh")
+    # facade modules under the reference's module names (registered first, so
+    # the reference's own `from .solver import ...` statements bind to them)
+    mesh_mod = types.ModuleType("fedheat.mesh")  # Mesh + the text parser / writer (meshio.py)
     mesh_mod.__dict__.update({k: v for k, v in vars(mesh).items() if not k.startswith("__")})
     for name in ("parse_mesh_text", "parse_mesh", "serialize_mesh_text", "serialize_mesh"):
         setattr(mesh_mod, name, getattr(meshio, name))
@@ -77,17 +73,25 @@ def _install_aliases() -> bool:
     gen_mod.__dict__.update({k: v for k, v in vars(meshgen).items() if not k.startswith("__")})
     gen_mod._TET_PATTERNS = list(meshgen.KUHN_PATTERNS)
     gen_mod._HEX_OFFSETS = meshgen.HEX_CORNER_OFFSETS
-    for name, mod in (("solver", solver), ("kernels", kernels), ("element", element), ("material", material),
-                      ("mesh", mesh_mod), ("meshgen", gen_mod), ("precompute", precompute), ("errors", errors),
-                      ("vtkio", vtkio)):
+    aliases = {"solver": solver, "kernels": kernels, "element": element, "material": material, "mesh": mesh_mod,
+               "meshgen": gen_mod, "precompute": precompute, "errors": errors, "vtkio": vtkio}
+    for name, mod in aliases.items():
         sys.modules[f"fedheat.{name}"] = mod
+    # the package itself is the reference's __init__ (a real file package, so
+    # importlib.resources finds the bundled scenarios); everything it does not
+    # find in sys.modules (scenario, and later oracle / cli / bench) loads from
+    # the installed reference as test infrastructure
+    spec = importlib.util.spec_from_file_location("fedheat", os.path.join(REF_PKG, "__init__.py"),
+                                                  submodule_search_locations=[REF_PKG])
+    pkg = importlib.util.module_from_spec(spec)
+    sys.modules["fedheat"] = pkg
+    spec.loader.exec_module(pkg)
+    for name, mod in aliases.items():
         setattr(pkg, name, mod)
-    for name in ("oracle", "scenario", "cli", "bench"):  # test infrastructure from the reference
-        spec = importlib.util.spec_from_file_location(f"fedheat.{name}", os.path.join(REF_PKG, f"{name}.py"))
-        mod = importlib.util.module_from_spec(spec)
-        sys.modules[f"fedheat.{name}"] = mod
-        spec.loader.exec_module(mod)
-        setattr(pkg, name, mod)
+    for name in ("oracle", "scenario", "cli", "bench"):
+        importlib.import_module(f"fedheat.{name}")
+    assert sys.modules["fedheat.solver"] is solver and pkg.ExplicitEngine is fh.ExplicitEngine
+    pkg.__fh_alias__ = True
     return True
 
 

@@ -20,9 +20,9 @@ two norms:
   rel_T    = max|T - T_ref| / max|T_ref|          (north_star's relative error)
   rel_rise = max|T - T_ref| / max|T_ref - T0|     (relative to the computed change)
 
-The gate is rel_T <= 1e-10 / 1e-4 and rel_rise <= 1e-9 / 1e-3 (the rise is
-~20-40x smaller than |T| over these runs; fp32 stores T itself with a 6e-8
-relative ulp).  With FH_PARITY_JSON set, every measured norm is appended to
+Both norms are gated at the north_star tolerance, 1e-10 (fp64) / 1e-4
+(fp32): the rise-normalised norm is the stricter one (the rise is 3-40x
+smaller than max |T| over these runs).  With FH_PARITY_JSON set, every measured norm is appended to
 that file (profiles/r2_parity_fullsize.json holds the GPU box's numbers).
 """
 
@@ -45,7 +45,7 @@ from paper_1909_05098_b200.sources import robin_lumps  # noqa: E402
 from oracle import oracle as orc  # noqa: E402
 
 TOL_T = {64: 1e-10, 32: 1e-4}
-TOL_RISE = {64: 1e-9, 32: 1e-3}
+TOL_RISE = {64: 1e-10, 32: 1e-4}
 T0 = 37.0
 
 

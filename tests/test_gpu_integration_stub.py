@@ -65,8 +65,13 @@ for tag in ("scen_td", "scen_twostage"):
     nodal = rng.uniform(0.4, 0.6, mesh.n_nodes)
     out = np.empty(packed.n_elements)
     kernels.element_mean_nodal(packed.conn_data, packed.conn_offs, nodal, out)
-    ref = np.array([sum(nodal[packed.conn_data[a:b]].tolist(), 0.0) / (b - a)
-                    for a, b in zip(packed.conn_offs[:-1], packed.conn_offs[1:])])
+    ref = np.empty(packed.n_elements)
+    for e in range(packed.n_elements):  # kernels.py:90-98: s = 0.0; s += ... in local-node order
+        a, b = int(packed.conn_offs[e]), int(packed.conn_offs[e + 1])
+        s = 0.0
+        for p in range(a, b):
+            s += float(nodal[packed.conn_data[p]])
+        ref[e] = s / (b - a)
     assert np.array_equal(out, ref), "element_mean_nodal"
 print("STUB-OK")
 """

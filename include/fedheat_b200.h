@@ -150,6 +150,20 @@ typedef struct {
   int32_t n_domains;              /* multi-GPU: domains the mesh is cut into (1, 2, 4 or 8) */
   int32_t domain_lo, domain_hi;   /* this engine owns domains [lo, hi) */
   int32_t slab_axis;              /* -1: recursive coordinate bisection; 0/1/2: domains are slabs */
+  /* Tuning knobs.  0 selects the measured default everywhere; the values are
+   * explicit so that no environment variable changes what the library does. */
+  int32_t exact_resident;   /* EXACT: 0 auto (resident many-steps-per-launch kernel when the mesh's
+                               per-CTA working set fits shared memory), 1 off (two launches per step),
+                               2 required (FH_ERR_CONFIG when it does not fit) */
+  int32_t resident_ctas;    /* resident path: CTA count (0: one per SM) */
+  int32_t tile_mode;        /* TILED hex accumulation mode + 1 (0: default) */
+  int32_t tile_stages;      /* TILED TMA ring depth (0: default 2) */
+  int32_t tet_rows;         /* TILED tet accumulator rows: 0 default, 1 or 4 */
+  int32_t launch_order;     /* TILED: 0 default, 1 partition (RCB) order, 2 longest tiles first */
+  int32_t kind_split;       /* TILED mixed meshes: 0 default (split hex-only tiles), 1 one launch */
+  int32_t hex_color;        /* TILED: 0 default, 1 colour-sort hex slots even when corner-unique */
+  int32_t first_touch;      /* TILED: 0 default (off), 1 first-touch node order inside tiles */
+  int32_t allow_nondeterministic; /* must be 1 for tile_mode = shared-memory atomics (5) */
 } fh_options;
 
 typedef struct {
@@ -235,8 +249,10 @@ typedef struct {
   int64_t n_parts, n_slots, n_nodes_owned, n_elements;
   int64_t step_bytes;      /* bytes the fused step streams from/to HBM (layout) */
   int64_t canonical_bytes; /* SURVEY 8(d) canonical bytes per step */
-  int32_t kernels_per_step;
+  int32_t kernels_per_step; /* launches per step; 0: the resident EXACT kernel runs many steps per launch */
   int32_t max_part_nodes;
+  int32_t resident_ctas;    /* EXACT: CTAs of the resident kernel (0: two launches per step) */
+  int32_t resident_threads; /* threads per resident CTA */
 } fh_layout;
 int fh_get_layout(fh_engine *e, fh_layout *out);
 

@@ -60,13 +60,18 @@ class FhBoundary(C.Structure):
     ]
 
 
+# fh_options tuning knobs (include/fedheat_b200.h); 0 = the measured default
+TUNING_FIELDS = ("exact_resident", "resident_ctas", "tile_mode", "tile_stages", "tet_rows", "launch_order",
+                 "kind_split", "hex_color", "first_touch", "allow_nondeterministic")
+
+
 class FhOptions(C.Structure):
     _fields_ = [
         ("precision", C.c_int32), ("assembly", C.c_int32), ("td_mode", C.c_int32), ("device", C.c_int32),
         ("runaway_limit", C.c_double), ("n_materials", C.c_int32), ("materials", C.POINTER(FhMaterial)),
         ("element_region", i32p), ("element_kfactor", f64p), ("part_nodes", C.c_int32),
         ("n_domains", C.c_int32), ("domain_lo", C.c_int32), ("domain_hi", C.c_int32), ("slab_axis", C.c_int32),
-    ]
+    ] + [(name, C.c_int32) for name in TUNING_FIELDS]
 
 
 class FhReport(C.Structure):
@@ -77,7 +82,8 @@ class FhReport(C.Structure):
 class FhLayout(C.Structure):
     _fields_ = [("n_parts", C.c_int64), ("n_slots", C.c_int64), ("n_nodes_owned", C.c_int64),
                 ("n_elements", C.c_int64), ("step_bytes", C.c_int64), ("canonical_bytes", C.c_int64),
-                ("kernels_per_step", C.c_int32), ("max_part_nodes", C.c_int32)]
+                ("kernels_per_step", C.c_int32), ("max_part_nodes", C.c_int32),
+                ("resident_ctas", C.c_int32), ("resident_threads", C.c_int32)]
 
 
 # every symbol include/fedheat_b200.h declares (checked by tests/test_native_abi.py)

@@ -10,6 +10,7 @@
 
 #include "fh_dist.h"
 #include "fh_tiled.cuh"
+#include "fh_resident.h"
 
 using namespace fh;
 
@@ -217,6 +218,16 @@ struct fh_engine {
   ExactArgs ex{};
   DBuf<double> A, kbar, cap, kb, qb, qm, qr, qstat, contrib, F, T, dir_vals_d, robin_hA_d, robin_hAT_d;
   DBuf<int32_t> dir_slot, robin_slot;
+  // resident small-mesh EXACT path (fh_resident.cu)
+  bool resident = false, res_stage_k = false;
+  int res_ctas = 0, res_threads = 0;
+  size_t res_smem = 0;
+  ResidentArgs res{};
+  DBuf<int32_t> r_cta_node, r_cta_halo, r_halo, r_cta_inc, r_inc_elem;
+  DBuf<uint16_t> r_lconn;
+  DBuf<uint8_t> r_info;
+  DBuf<double> T1;
+  DBuf<unsigned long long> r_bar;
   // tiled
   Partition part;
   DBuf<int64_t> old_of_new, new_of_old;
@@ -311,9 +322,9 @@ int default_part_nodes(int precision, int64_t n_tet, int64_t n_hex) {
 
 // Tet-only meshes: colour classes with up to 4 writes per node (4 accumulator
 // rows, ~4x larger classes -> fewer colour phases per 256-slot batch).
-int default_tet_rows(int64_t n_tet, int64_t n_hex) {
+int default_tet_rows(int64_t n_tet, int64_t n_hex, int knob) {
   int r = (n_tet > 0 && n_hex == 0) ? 4 : 1;
-  if (const char *env = getenv("FH_TET_ROWS")) r = atoi(env) > 1 ? 4 : 1;
+  if (knob > 0) r = knob > 1 ? 4 : 1;  // fh_options.tet_rows
   return r;
 }
 
@@ -474,6 +485,66 @@ void setup_exact(fh_engine *e, const fh_boundary &b) {
   FH_CUDA(cudaStreamSynchronize(s));
 }
 
+// The resident path (fh_resident.cu) when every CTA's working set fits
+// shared memory and the grid stays co-resident (one CTA per SM by default).
+void setup_resident(fh_engine *e, const std::vector<int32_t> &conn, const std::vector<int32_t> &offs,
+                    const std::vector<int32_t> &pos) {
+  const fh_options &o = e->opts;
+  if (o.exact_resident == 1) return;
+  int sms = 148, smem_optin = 227 * 1024;
+  FH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
+  FH_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+  const bool stage_k = e->td && !(o.n_materials > 1 && o.element_region);
+  const int ctas = o.resident_ctas > 0 ? o.resident_ctas : sms;
+  ResidentPlan P;
+  bool ok = build_resident_plan(e->V, e->n_tet, FH_CHUNK_SIZE, conn, offs, pos, ctas, stage_k, !e->td,
+                                (size_t)smem_optin - 1024, P);
+  if (ok) ok = (int64_t)resident_occupancy(e->td, stage_k, P.threads, P.smem) * sms >= P.n_cta;
+  if (!ok) {
+    if (o.exact_resident == 2) fail(FH_ERR_CONFIG, "the resident EXACT path does not fit this mesh");
+    return;
+  }
+  cudaStream_t s = e->stream;
+  e->r_cta_node.upload(P.cta_node, s);
+  e->r_cta_halo.upload(P.cta_halo, s);
+  e->r_halo.upload(P.halo_nodes.empty() ? std::vector<int32_t>{0} : P.halo_nodes, s);
+  e->r_cta_inc.upload(P.cta_inc, s);
+  e->r_inc_elem.upload(P.inc_elem, s);
+  e->r_lconn.upload(P.inc_lconn, s);
+  e->r_info.upload(P.inc_info, s);
+  e->T1.alloc(e->V);
+  e->r_bar.alloc(1);
+  e->r_bar.zero(s);
+  ResidentArgs &r = e->res;
+  std::memset(&r, 0, sizeof(r));
+  r.cta_node = e->r_cta_node.p;
+  r.cta_halo = e->r_cta_halo.p;
+  r.halo_nodes = e->r_halo.p;
+  r.cta_inc = e->r_cta_inc.p;
+  r.inc_lconn = e->r_lconn.p;
+  r.inc_elem = e->r_inc_elem.p;
+  r.inc_info = e->r_info.p;
+  r.off_K = (uint32_t)P.off_K;
+  r.off_A = (uint32_t)P.off_A;
+  r.off_C = (uint32_t)P.off_C;
+  r.off_Kb = (uint32_t)P.off_Kb;
+  r.off_L = (uint32_t)P.off_L;
+  r.off_E = (uint32_t)P.off_E;
+  r.off_I = (uint32_t)P.off_I;
+  r.off_H = (uint32_t)P.off_H;
+  r.off_N = (uint32_t)P.off_N;
+  r.off_O = (uint32_t)P.off_O;
+  r.T0 = e->T.p;
+  r.T1 = e->T1.p;
+  r.bar = e->r_bar.p;
+  e->resident = true;
+  e->res_stage_k = stage_k;
+  e->res_ctas = P.n_cta;
+  e->res_threads = P.threads;
+  e->res_smem = P.smem;
+  FH_CUDA(cudaStreamSynchronize(s));
+}
+
 // ---------------------------------------------------------------------------
 template <typename S>
 void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const double *G_dev) {
@@ -502,10 +573,10 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
                                                 e->refit_per_sm);
   const int target_used = pin.target_part_nodes;
   pin.batch = kBatch;
-  // layout tuning knobs (scripts/sweep.py): hex colour order, first-touch node order
-  if (const char *env = getenv("FH_HEX_COLOR")) pin.hex_color = atoi(env);
-  if (const char *env = getenv("FH_FIRST_TOUCH")) pin.first_touch = atoi(env);
-  pin.tet_rows = default_tet_rows(e->n_tet, e->n_hex);
+  // layout tuning knobs (fh_options; scripts/sweep.py): hex colour order, first-touch node order
+  pin.hex_color = o.hex_color;
+  pin.first_touch = o.first_touch;
+  pin.tet_rows = default_tet_rows(e->n_tet, e->n_hex, o.tet_rows);
   pin.n_domains = std::max(1, o.n_domains);
   pin.slab_axis = o.slab_axis;
   build_partition(pin, e->part);
@@ -542,7 +613,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   const int per_sm = e->refit_per_sm > 0 ? e->refit_per_sm
                                          : (sizeof(S) == 4 ? (e->n_hex == 0 ? 5 : 4) : 2);
   bool lpt = (double)plist.size() / ((double)sms * per_sm) < 6.0;
-  if (const char *env = getenv("FH_LPT")) lpt = atoi(env) != 0;
+  if (o.launch_order) lpt = o.launch_order == 2;
   if (lpt) {
     auto work = [&](int32_t p) { return (int64_t)P.part_tet_count[p] + 2 * (int64_t)P.part_hex_count[p]; };
     auto by_work = [&](int32_t a, int32_t b) { return work(a) > work(b); };
@@ -552,7 +623,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   // mixed meshes: inside each launch range the tiles holding tets come first,
   // so the hex-only tiles can run the leaner hex-only kernel instance
   bool split = e->n_tet > 0 && e->n_hex > 0;
-  if (const char *env = getenv("FH_KIND_SPLIT")) split = split && atoi(env) != 0;
+  if (o.kind_split == 1) split = false;
   st->n_mixed_b = st->n_boundary;
   st->n_mixed_i = st->n_parts_local - st->n_boundary;
   if (split) {
@@ -603,12 +674,16 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   // 1% faster than one row; fp64 keeps one row (shared memory)
   const int corner_mode = sizeof(S) == 4 ? kModeCornerPhase2 : kModeCornerPhase;
   int mode = P.corner_unique ? corner_mode : (hex_colour_ok ? kModeColored : kModeRanked);
-  if (const char *env = getenv("FH_TILE_MODE")) {
-    const int m = atoi(env);
+  if (o.tile_mode > 0) {  // fh_options.tile_mode = mode + 1 (explicit, checked)
+    const int m = o.tile_mode - 1;
+    if (m == kModeSharedAtomic && !o.allow_nondeterministic)
+      fail(FH_ERR_CONFIG, "tile_mode shared-memory atomics is non-deterministic: set allow_nondeterministic");
     if (m == kModeRanked || m == kModeSharedAtomic || (m == kModeColored && hex_colour_ok) ||
         ((m == kModeCornerPhase || m == kModeCornerSlot || m == kModeCornerPhase2 || m == kModeCornerPhase4) &&
          P.corner_unique))
       mode = m;
+    else
+      fail(FH_ERR_CONFIG, "tile_mode " + std::to_string(o.tile_mode) + " does not apply to this mesh");
   }
   // `mode` is the hex mode (kernel template); tets never are corner-unique and
   // always use colour phases (or ranked phases if the colouring overflowed)
@@ -792,7 +867,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   // FH_TILE_MODE (0/1/2) and FH_TILE_STAGES override the defaults (tuning knobs)
   st->mode = mode;
   g.n_stages = 2;  // measured best on cfg4 (scripts/sweep.py)
-  if (const char *env = getenv("FH_TILE_STAGES")) g.n_stages = std::min(kMaxStages, std::max(1, atoi(env)));
+  if (o.tile_stages > 0) g.n_stages = std::min(kMaxStages, o.tile_stages);
   g.smem_T = (int)al(2 * sizeof(S) * (size_t)std::max(1, P.max_local_nodes));
   // +1: the trash slot of the corner-phase accumulation
   const int rows = std::max(st->mode == kModeCornerSlot ? 8 : st->mode == kModeCornerPhase4 ? 4
@@ -1009,8 +1084,62 @@ void exact_run(fh_engine *e, int64_t nsteps, double dt) {
   }
 }
 
+// would the active-load signature differ at step start time t?
+bool loads_differ_at(const fh_engine *e, double t) {
+  for (size_t l = 0; l < e->load_power.size(); ++l) {
+    const uint8_t on = (e->load_t0[l] <= t && t < e->load_t1[l]);
+    if (on != e->load_sig[l]) return true;
+  }
+  return false;
+}
+
+// EXACT on the resident kernel: one launch per segment of steps whose active
+// loads do not change (q_r is re-uploaded between segments, as exact_run does
+// before the step where a window opens or closes)
+void resident_exact_run(fh_engine *e, int64_t nsteps, double dt) {
+  int64_t k = 0;
+  while (k < nsteps) {
+    const double t = e->time;
+    upload_qr(e, t);
+    if (!e->td && !e->frozen) {
+      exact_props(e->ex, e->T.p, e->stream);
+      e->frozen = true;
+    }
+    int64_t seg = nsteps - k;
+    if (!e->load_power.empty()) {
+      seg = 1;
+      while (k + seg < nsteps && !loads_differ_at(e, (double)(e->step_index + seg) * dt)) ++seg;
+    }
+    ResidentArgs r = e->res;
+    r.g = e->ex;
+    r.step0 = e->step_index;
+    r.nsteps = seg;
+    r.time0 = t;
+    r.dt = dt;
+    r.probes = e->probes.p;
+    r.n_probes = e->n_probes;
+    r.probe_interval = e->probe_interval;
+    r.rec0 = e->n_rec;
+    r.rec_cap = e->probe_cap;
+    r.probe_out = e->probe_hist.p;
+    e->r_bar.zero(e->stream);
+    resident_run(r, e->res_ctas, e->res_threads, e->res_smem, e->td, e->res_stage_k, e->stream);
+    for (int64_t j = 0; j < seg; ++j) {  // the records the kernel writes (exact_run's bookkeeping)
+      e->step_index += 1;
+      if (e->n_probes && e->step_index % e->probe_interval == 0 && e->n_rec < e->probe_cap) {
+        e->probe_steps.push_back(e->step_index);
+        e->n_rec++;
+      }
+    }
+    e->time = (double)e->step_index * dt;
+    k += seg;
+  }
+}
+
 void run_steps(fh_engine *e, int64_t nsteps, double dt) {
-  if (e->assembly == FH_ASSEMBLY_EXACT)
+  if (e->assembly == FH_ASSEMBLY_EXACT && e->resident && !e->dir_runaway)
+    resident_exact_run(e, nsteps, dt);
+  else if (e->assembly == FH_ASSEMBLY_EXACT)
     exact_run(e, nsteps, dt);
   else if (e->precision == 32)
     tiled_run<float>(e, nsteps, dt);
@@ -1254,6 +1383,7 @@ int fh_create(const fh_mesh *mesh, const fh_boundary *bnd, const fh_options *opt
   e->stage.alloc(e->V);
   if (e->assembly == FH_ASSEMBLY_EXACT) {
     setup_exact(e.get(), *bnd);
+    setup_resident(e.get(), conn, offs, pos);
   } else if (e->precision == 32) {
     setup_tiled<float>(e.get(), *mesh, *bnd, G.p);
   } else {
@@ -1684,7 +1814,9 @@ int fh_get_layout(fh_engine *e, fh_layout *out) {
   if (!e->sources.empty()) canon += e->V * 3 * s;
   out->canonical_bytes = canon;
   if (e->assembly == FH_ASSEMBLY_EXACT) {
-    out->kernels_per_step = 2;
+    out->kernels_per_step = e->resident ? 0 : 2;
+    out->resident_ctas = e->resident ? e->res_ctas : 0;
+    out->resident_threads = e->resident ? e->res_threads : 0;
     out->n_slots = e->E;
     out->n_nodes_owned = e->V;
     // conn + A + contrib w/r + csr + node streams
@@ -2008,10 +2140,10 @@ int fh_plan_create(const fh_mesh *mesh, const fh_boundary *bnd, const fh_options
     pin.target_part_nodes = wave_fit_part_nodes(pin.target_part_nodes, mesh->n_nodes, std::max(1, opts->n_domains),
                                                 opts->precision, mesh->n_tets, mesh->n_hexes, opts->device);
   pin.batch = kBatch;
-  // layout tuning knobs (scripts/sweep.py): hex colour order, first-touch node order
-  if (const char *env = getenv("FH_HEX_COLOR")) pin.hex_color = atoi(env);
-  if (const char *env = getenv("FH_FIRST_TOUCH")) pin.first_touch = atoi(env);
-  pin.tet_rows = default_tet_rows(mesh->n_tets, mesh->n_hexes);
+  // layout tuning knobs (fh_options): hex colour order, first-touch node order
+  pin.hex_color = opts->hex_color;
+  pin.first_touch = opts->first_touch;
+  pin.tet_rows = default_tet_rows(mesh->n_tets, mesh->n_hexes, opts->tet_rows);
   pin.n_domains = std::max(1, opts->n_domains);
   pin.slab_axis = opts->slab_axis;
   build_partition(pin, pl->P);

@@ -13,29 +13,9 @@
 //                  element order; partials added in chunk order), fused with
 //                  the lumped update of kernels.py:137-142, the Dirichlet
 //                  overwrite and the runaway check of solver.py:364-382.
-#include "fh_exact.h"
+#include "fh_exact_dev.cuh"
 
 namespace fh {
-
-__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ double dvd(double a, double b) { return __ddiv_rn(a, b); }
-
-constexpr unsigned long long kNoFail = ~0ull;
-
-__device__ __forceinline__ int64_t eoff(const ExactArgs &g, int64_t e) {
-  if (g.conn_offs) return g.conn_offs[e];
-  return e < g.n_tet ? 4 * e : 4 * g.n_tet + 8 * (e - g.n_tet);
-}
-__device__ __forceinline__ int64_t moff(const ExactArgs &g, int64_t e) {
-  if (g.mat_offs) return g.mat_offs[e];
-  return e < g.n_tet ? 16 * e : 16 * g.n_tet + 64 * (e - g.n_tet);
-}
-__device__ __forceinline__ int64_t elem_of_pos(const ExactArgs &g, int64_t p) {
-  if (g.elem_of) return g.elem_of[p];
-  return p < 4 * g.n_tet ? p / 4 : g.n_tet + (p - 4 * g.n_tet) / 8;
-}
 
 __device__ __forceinline__ double elem_kbar(const ExactArgs &g, int64_t e, const double *__restrict__ T) {
   const int64_t lo = eoff(g, e), hi = eoff(g, e + 1);
@@ -101,17 +81,6 @@ __device__ __forceinline__ double chunked_gather(const ExactArgs &g, int64_t i) 
   return total;
 }
 
-__device__ double source_density(const fh_source &s, double x, double y, double z, double t) {
-  if (!(s.t0 <= t && t < s.t1)) return 0.0;
-  const double d0 = x - (s.x0[0] + s.vel[0] * t), d1 = y - (s.x0[1] + s.vel[1] * t),
-               d2 = z - (s.x0[2] + s.vel[2] * t);
-  const double r2 = (d0 * d0 + d1 * d1) + d2 * d2;
-  if (s.kind == FH_SOURCE_GAUSSIAN) return s.amp * exp(-r2 / (2.0 * s.sigma * s.sigma));
-  double q = s.cap;
-  if (r2 > 0.0) q = fmin(q, s.amp / (4.0 * 3.14159265358979323846 * r2));
-  return q;
-}
-
 __global__ void k_exact_node(ExactArgs g, double *__restrict__ T, double dt, double t_start,
                              unsigned long long step_no, int td) {
   if (g.flag && g.flag->step < step_no) return;
@@ -120,41 +89,7 @@ __global__ void k_exact_node(ExactArgs g, double *__restrict__ T, double dt, dou
   if (i < g.V) {
     const double F = chunked_gather(g, i);
     if (g.F) g.F[i] = F;
-    const double x = T[i];
-    const double v = g.node_vol[i];
-    const Mat<double> &m = g.mats.m[g.node_region ? g.node_region[i] : 0];
-    double cap, kb, qb;
-    if (td) {
-      cap = mul(mul(interp_rn(m.rho, x), interp_rn(m.c, x)), v);
-      if (m.td_perf) {
-        kb = mul(mul(interp_rn(m.wb, x), m.cb), v);
-        qb = mul(kb, m.Ta);
-      } else {
-        kb = g.kb[i];
-        qb = g.qb[i];
-      }
-    } else {
-      cap = g.cap[i];
-      kb = g.kb[i];
-      qb = g.qb[i];
-    }
-    double rate = add(add(add(sub(F, mul(kb, x)), qb), g.qm[i]), g.qr[i]);
-    if (g.q_static) rate = add(rate, g.q_static[i]);
-    if (g.n_src) {
-      double q = 0.0;
-      for (int s = 0; s < g.n_src; ++s)
-        q += source_density(g.src[s], g.xyz[3 * i], g.xyz[3 * i + 1], g.xyz[3 * i + 2], t_start);
-      rate = add(rate, mul(q, v));
-    }
-    if (g.robin_slot) {
-      const int32_t rs = g.robin_slot[i];
-      if (rs >= 0) rate = add(sub(rate, mul(g.robin_hA[rs], x)), g.robin_hAT[rs]);
-    }
-    double xn = add(x, dvd(mul(dt, rate), cap));
-    if (g.dir_slot) {
-      const int32_t ds = g.dir_slot[i];
-      if (ds >= 0) xn = g.dir_vals[ds];
-    }
+    const double xn = exact_update(g, i, F, T[i], dt, t_start, td);
     T[i] = xn;
     bad = !isfinite(xn) || fabs(xn) > g.runaway_limit;
   }

@@ -42,12 +42,13 @@ class Plan:
 
     def __init__(self, mesh, material, boundary: BoundarySpec | None = None, *, world: int = 1, rank: int = 0,
                  n_domains: int = DEFAULT_DOMAINS, slab_axis: int = -1, part_nodes: int = 0, precision: int = 32,
-                 robin=()):
+                 robin=(), tuning=None):
         self.mesh = mesh
         self.boundary = resolve_boundary(boundary or BoundarySpec(), mesh)
         fm, fb, fo, keep, _ = native_inputs(mesh, self.boundary, [material], robin=robin, precision=precision,
                                             assembly="tiled", part_nodes=part_nodes, n_domains=n_domains,
-                                            domains=domain_range(rank, world, n_domains), slab_axis=slab_axis)
+                                            domains=domain_range(rank, world, n_domains), slab_axis=slab_axis,
+                                            tuning=tuning)
         self._keep = keep
         h = C.c_void_p()
         N.check(N.lib().fh_plan_create(C.byref(fm), C.byref(fb), C.byref(fo), world, rank, C.byref(h)))

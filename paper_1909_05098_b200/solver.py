@@ -217,7 +217,7 @@ def _source_array(sources):
 
 def native_inputs(mesh, bnd, materials, *, sources=(), robin=(), kfactor=None, element_region=None,
                   td_mode=False, precision=64, assembly="exact", runaway_limit=DEFAULT_RUNAWAY_LIMIT, device=0,
-                  part_nodes=0, n_domains=1, domains=None, slab_axis=-1):
+                  part_nodes=0, n_domains=1, domains=None, slab_axis=-1, tuning=None):
     """C-ABI descriptors (fh_mesh, fh_boundary, fh_options) for a problem.
 
     Returns (mesh, boundary, options, keep, robin) -- ``keep`` holds the numpy
@@ -283,6 +283,10 @@ def native_inputs(mesh, bnd, materials, *, sources=(), robin=(), kfactor=None, e
     fo.n_domains = int(n_domains)
     lo, hi = domains if domains is not None else (0, int(n_domains))
     fo.domain_lo, fo.domain_hi, fo.slab_axis = int(lo), int(hi), int(slab_axis)
+    for name, value in (tuning or {}).items():
+        if name not in N.TUNING_FIELDS:
+            raise ConfigError(f"unknown tuning knob {name!r} (known: {', '.join(N.TUNING_FIELDS)})")
+        setattr(fo, name, int(value))
     return fm, fb, fo, keep, robin_out
 
 
@@ -293,7 +297,7 @@ class ExplicitEngine:
                  td_mode: bool | None = None, runaway_limit: float = DEFAULT_RUNAWAY_LIMIT,
                  dt_recheck_interval: int = DEFAULT_DT_RECHECK, precision: int = 64, assembly: str = "exact",
                  sources=(), robin=(), kfactor=None, materials=None, element_region=None, device: int = 0,
-                 part_nodes: int = 0, n_domains: int = 1, domains=None, slab_axis: int = -1):
+                 part_nodes: int = 0, n_domains: int = 1, domains=None, slab_axis: int = -1, tuning=None):
         t_begin = _time.perf_counter()
         self.mesh = mesh
         self.material = material
@@ -318,7 +322,7 @@ class ExplicitEngine:
             mesh, self.boundary, self.materials, sources=self.sources, robin=robin, kfactor=kfactor,
             element_region=element_region, td_mode=self.td_mode, precision=self.precision, assembly=assembly,
             runaway_limit=self.runaway_limit, device=device, part_nodes=part_nodes, n_domains=n_domains,
-            domains=domains, slab_axis=slab_axis)
+            domains=domains, slab_axis=slab_axis, tuning=tuning)
         self._keep = keep
         self._h = None
         handle = C.c_void_p()

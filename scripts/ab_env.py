@@ -1,4 +1,4 @@
-"""Same-box A/B of an engine environment knob: python scripts/ab_env.py VAR v0 v1 cfg...
+"""Same-box A/B of an engine tuning knob (fh_options): python scripts/ab_env.py KNOB v0 v1 cfg...
 Device ms per step for each value (2 reps) and a bitwise comparison of the fields."""
 import ctypes as C
 import json
@@ -18,9 +18,9 @@ for cfg in cfgs:
     for rep in range(2):
         res = {}
         for v in vals:
-            os.environ[var] = v
             eng = fh.ExplicitEngine(prob.mesh, prob.material, prob.boundary, assembly="tiled", n_domains=8,
-                                    slab_axis=2 if cfg == "cfg4" else -1, **prob.engine_kwargs())
+                                    slab_axis=2 if cfg == "cfg4" else -1, tuning={var: int(v)},
+                                    **prob.engine_kwargs())
             dt = 0.9 * eng.critical_dt(37.0)
             st = eng.initial_state(37.0)
             L, h = eng._L, eng._h

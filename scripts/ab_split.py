@@ -1,5 +1,5 @@
 """Same-box A/B of the tile-kind split on a mixed mesh (cfg5): device time per
-step with FH_KIND_SPLIT=0 / 1 and a bitwise comparison of the fields."""
+step with tuning kind_split=1 (one launch) / 0 (split, default) and a bitwise comparison of the fields."""
 import ctypes as C
 import json
 import os
@@ -16,9 +16,8 @@ prob = bench.make_problem(sys.argv[1] if len(sys.argv) > 1 else "cfg5", 0, 32)
 out = {}
 for rep in range(2):
     for split in ("0", "1"):
-        os.environ["FH_KIND_SPLIT"] = split
         eng = fh.ExplicitEngine(prob.mesh, prob.material, prob.boundary, assembly="tiled", n_domains=8,
-                                **prob.engine_kwargs())
+                                tuning={"kind_split": 1 if split == "0" else 0}, **prob.engine_kwargs())
         dt = 0.9 * eng.critical_dt(37.0)
         st = eng.initial_state(37.0)
         L, h = eng._L, eng._h

@@ -1,6 +1,9 @@
 """Tuning sweep of the fused step on one workload (GPU): tile size x
-accumulation mode x TMA ring depth.  The mesh is built once; each variant
-gets its own engine.  Prints one line per variant."""
+accumulation mode x TMA ring depth (fh_options tuning knobs; --tuning adds
+more, e.g. --tuning first_touch=1,hex_color=1).  The mesh is built once; each
+variant gets its own engine.  Prints one line per variant.  Mode ids are the
+kernel's (0 ranked, 1 corner phases, 3 colour phases, 4 shared atomics, 5 two-row
+corner phases); mode -1 = the engine default."""
 import argparse
 import ctypes as C
 import json
@@ -23,6 +26,7 @@ ap.add_argument("--parts", default="768,1024")
 ap.add_argument("--modes", default="1,2")
 ap.add_argument("--stages", default="2,3")
 ap.add_argument("--steps", type=int, default=50)
+ap.add_argument("--tuning", default="")
 ap.add_argument("--check", action="store_true", help="compare each variant's field with the first one's")
 args = ap.parse_args()
 
@@ -33,10 +37,12 @@ ref = None
 for pn in [int(x) for x in args.parts.split(",")]:
     for mode in [int(x) for x in args.modes.split(",")]:
         for stg in [int(x) for x in args.stages.split(",")]:
-            os.environ["FH_TILE_MODE"] = str(mode)
-            os.environ["FH_TILE_STAGES"] = str(stg)
+            tuning = {"tile_mode": mode + 1, "tile_stages": stg}
+            tuning.update({k: int(v) for k, v in (kv.split("=") for kv in args.tuning.split(",") if kv)})
+            if mode == 4:
+                tuning["allow_nondeterministic"] = 1
             eng = fh.ExplicitEngine(prob.mesh, prob.material, prob.boundary, assembly="tiled", part_nodes=pn,
-                                    **prob.engine_kwargs())
+                                    tuning=tuning, **prob.engine_kwargs())
             dt = 0.9 * eng.critical_dt(37.0)
             st = eng.initial_state(37.0)
             L, h = eng._L, eng._h

@@ -57,7 +57,7 @@ def restated_partition(mesh, dirichlet, robin, n_domains, target, slab_axis=-1):
 @pytest.mark.parametrize("kind,div,ndom,target,slab", [("hex", 9, 1, 100, -1), ("tet", 6, 2, 64, -1),
                                                       ("hex", 10, 8, 150, -1), ("hex", 12, 4, 200, 2),
                                                       ("tet", 5, 8, 40, 2)])
-def test_partition_matches_restatement_bitwise(kind, div, ndom, target, slab, monkeypatch):
+def test_partition_matches_restatement_bitwise(kind, div, ndom, target, slab):
     mesh = fh.jittered_cube_mesh(kind, div, 0.1, 0.2, seed=div)
     bnd = fh.BoundarySpec(dirichlet=(("z0", 37.0), ("x1", 37.0)))
     # default (no first-touch pass): the order is exactly (part, class, original id)
@@ -67,8 +67,8 @@ def test_partition_matches_restatement_bitwise(kind, div, ndom, target, slab, mo
     assert np.array_equal(plan0.new_to_old, n2o)
     assert np.array_equal(plan0.part_node_start, bounds)
     # first-touch order: same tiles and class ranges, nodes permuted inside each class
-    monkeypatch.setenv("FH_FIRST_TOUCH", "1")
-    plan = Plan(mesh, MAT, bnd, world=1, rank=0, n_domains=ndom, part_nodes=target, slab_axis=slab)
+    plan = Plan(mesh, MAT, bnd, world=1, rank=0, n_domains=ndom, part_nodes=target, slab_axis=slab,
+                tuning={"first_touch": 1})
     assert np.array_equal(plan.part_node_start, bounds)
     cls = np.zeros(mesh.n_nodes, np.int64)
     cls[dn] = 2
@@ -77,16 +77,16 @@ def test_partition_matches_restatement_bitwise(kind, div, ndom, target, slab, mo
         assert np.array_equal(cls[a], cls[b])  # class ranges kept
         assert np.array_equal(np.sort(a), np.sort(b))
     # same input -> same plan
-    again = Plan(mesh, MAT, bnd, world=1, rank=0, n_domains=ndom, part_nodes=target, slab_axis=slab)
+    again = Plan(mesh, MAT, bnd, world=1, rank=0, n_domains=ndom, part_nodes=target, slab_axis=slab,
+                 tuning={"first_touch": 1})
     assert np.array_equal(again.new_to_old, plan.new_to_old)
 
 
-def test_first_touch_order_makes_batch_gathers_contiguous(monkeypatch):
+def test_first_touch_order_makes_batch_gathers_contiguous():
     """Structured hex tile: corner a of consecutive slots of a batch maps to
     consecutive node ids (csrc/fh_partition.cpp step 4b)."""
     mesh = fh.generate_cube_mesh("hex", 12, 0.1)
-    monkeypatch.setenv("FH_FIRST_TOUCH", "1")
-    plan = Plan(mesh, MAT, n_domains=1, part_nodes=4096)
+    plan = Plan(mesh, MAT, n_domains=1, part_nodes=4096, tuning={"first_touch": 1})
     assert plan.info["n_parts"] == 1
     o2n = np.empty(mesh.n_nodes, np.int64)
     o2n[plan.new_to_old] = np.arange(mesh.n_nodes)
@@ -97,7 +97,7 @@ def test_first_touch_order_makes_batch_gathers_contiguous(monkeypatch):
     assert np.mean(steps == 1) > 0.9
 
 
-def test_structured_hex_is_corner_unique_and_tets_are_coloured(monkeypatch):
+def test_structured_hex_is_corner_unique_and_tets_are_coloured():
     hexm = fh.generate_cube_mesh("hex", 8, 0.1)
     assert Plan(hexm, MAT, part_nodes=100).info["corner_unique"] == 1
     tetm = fh.generate_cube_mesh("tet", 20, 0.1)
@@ -110,8 +110,7 @@ def test_structured_hex_is_corner_unique_and_tets_are_coloured(monkeypatch):
     assert info["max_nph_tet"] <= 4
     rows4 = info["sum_nph_tet"]
     # one row: one write per node and class -> >= 24 colours, more phases
-    monkeypatch.setenv("FH_TET_ROWS", "1")
-    info1 = Plan(tetm, MAT, part_nodes=1536).info
+    info1 = Plan(tetm, MAT, part_nodes=1536, tuning={"tet_rows": 1}).info
     assert info1["colored_ok"] == 1 and 24 <= info1["max_colors"] <= 64
     assert info1["max_nph_tet"] <= 8 and info1["sum_nph_tet"] > rows4
     hexm = fh.jittered_cube_mesh("hex", 6, 0.1, 0.1, seed=1)

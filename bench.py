@@ -16,8 +16,10 @@ per-step input (1.1 GB of slot + node streams for cfg4) is larger than the
 through the public C ABI with host buffers (pinned host T in, one step,
 host T out, every step; on one GPU fh_step_host_async double-buffers the
 host I/O so step k's download overlaps step k+1's upload).  ``--impl reference`` times the CPU oracle
-(restated reference path, oracle/fh_oracle.c, all host threads) on a bounded
-sample of the same workload family.
+(restated reference path, oracle/fh_oracle.c, all host threads) on the same
+full workload (same mesh, boundary, sources, dt), one oracle step per bench
+step, and (cfg4) the unmodified numba reference from baseline/_ref on the
+largest cube its chunk buffers fit (128^3), labelled as such.
 """
 
 from __future__ import annotations
@@ -48,7 +50,8 @@ def parse():
     ap.add_argument("--part-nodes", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-div", type=int, default=0)
+    ap.add_argument("--numba-divisions", type=int, default=128,
+                    help="reference arm, cfg4: also time the unmodified numba reference on this cube (0: skip)")
     return ap.parse_args()
 
 
@@ -129,62 +132,130 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_oracle_rate(name, divisions, steps, threads=None, per_step=False):
-    """Time the CPU oracle (restated reference path) on a bounded sample."""
-    from oracle import oracle as orc
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    prob = make_problem(name, divisions)
-    mesh = prob.mesh
+
+def oracle_for(prob):
+    """The CPU oracle (restated reference path, oracle/fh_oracle.c) on `prob`'s
+    full mesh and boundary, with the dt the GPU arm uses (0.9 x Gershgorin)."""
+    from oracle import oracle as orc
     from paper_1909_05098_b200.solver import resolve_boundary
     from paper_1909_05098_b200.sources import robin_lumps
 
+    mesh = prob.mesh
     rb = resolve_boundary(prob.boundary, mesh)
-    robin = None
-    if prob.robin:
-        robin = robin_lumps(mesh, prob.robin[0], exclude=rb.dirichlet_nodes)
-    if threads:
-        orc.set_threads(threads)
-    ora = orc.OracleModel(mesh, prob.materials or prob.material, dirichlet=(rb.dirichlet_nodes, rb.dirichlet_values),
-                          sources=[s.as_dict() for s in prob.sources], robin=robin, kfactor=prob.kfactor,
-                          elem_region=prob.element_region, td_mode=prob.td_mode)
-    ora.initial_state(37.0)
+    robin = robin_lumps(mesh, prob.robin[0], exclude=rb.dirichlet_nodes) if prob.robin else None
+    def model(sources):
+        return orc.OracleModel(mesh, prob.materials or prob.material,
+                               dirichlet=(rb.dirichlet_nodes, rb.dirichlet_values),
+                               sources=[s.as_dict() for s in sources], robin=robin, kfactor=prob.kfactor,
+                               elem_region=prob.element_region, td_mode=prob.td_mode)
+
+    ora = model(prob.sources)
     dt = 0.9 * ora.critical_dt(np.full(mesh.n_nodes, 37.0))
-    ora.step(dt, 1)  # warm-up
-    if per_step:
-        times = []
-        for _ in range(steps):
-            t0 = time.perf_counter()
-            ora.step(dt, 1)
-            times.append(time.perf_counter() - t0)
-        return times, mesh.n_elements, orc.max_threads()
-    t0 = time.perf_counter()
-    ora.step(dt, steps)
-    el = time.perf_counter() - t0
-    return mesh.n_elements * steps / el, el, mesh.n_elements, orc.max_threads()
+    if prob.name == "cfg4":  # the moving source of the fast arm depends on dt (run_sources)
+        del ora
+        ora = model(run_sources(prob, dt))
+    ora.initial_state(37.0)
+    return ora, dt, orc.max_threads()
+
+
+def run_sources(prob, dt):
+    """cfg4's moving Gaussian covers its seeded segment over the run's steps."""
+    import paper_1909_05098_b200 as fh
+
+    a, b = (np.asarray(v) for v in prob.notes["path"])
+    return [fh.GaussianSource(amp=5.0e6, sigma=0.005, x0=tuple(a), vel=tuple((b - a) / (prob.steps * dt)), t0=0.0)]
+
+
+def oracle_step_times(ora, dt, steps):
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        ora.step(dt, 1)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def numba_reference_rate(divisions, steps):
+    """The UNMODIFIED reference (fedheat, numba, baseline/_ref) through its own
+    public API on the largest cfg4-family cube its O(E*V) chunk buffers allow on
+    the host: TD laws of cfg2, Dirichlet 37 C on every
+    face, all host threads.  The reference has no k-factor or moving source."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "fedheat")):
+        return {"unavailable": "baseline/_ref not installed"}
+    code = f"""
+import json, os, sys, time
+sys.path.insert(0, {ref!r})
+import numpy as np
+import fedheat as fh
+mesh = fh.generate_cube_mesh("hex", {divisions}, 0.1)
+lin = lambda y0, s: fh.PropertyCurve(temperatures=np.array([0.0, 2000.0]), values=np.array([y0 * (1 + s * (0 - 37)), y0 * (1 + s * (2000 - 37))]))
+mat = fh.TissueMaterial(density=fh.PropertyCurve(temperatures=np.array([0.0]), values=np.array([1060.0])), specific_heat=lin(3600.0, -0.0005),
+                        conductivity=lin(0.5, 0.0013), perfusion_rate=0.525, blood_specific_heat=3640.0,
+                        arterial_temperature=37.0, metabolic_rate=420.0)
+bnd = fh.BoundarySpec(dirichlet=tuple((f, 37.0) for f in ("x0", "x1", "y0", "y1", "z0", "z1")))
+eng = fh.ExplicitEngine(mesh, mat, bnd)
+nw = os.cpu_count()
+eng.run(37.0, steps=2, auto_dt_safety=0.9, workers=nw)  # numba compile + buffers
+res = eng.run(37.0, steps={steps}, auto_dt_safety=0.9, workers=nw)
+print(json.dumps({{"per_step_s": res.timings["per_step_s"], "elements": mesh.n_elements, "workers": res.workers}}))
+"""
+    env = dict(os.environ)
+    env.setdefault("NUMBA_CACHE_DIR", "/tmp/fh_numba_cache")
+    env["NUMBA_NUM_THREADS"] = str(os.cpu_count())
+    try:
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900, env=env)
+        d = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as ex:  # noqa: BLE001
+        err = (out.stderr.strip().splitlines() or [""])[-1] if "out" in locals() else ""
+        return {"unavailable": f"reference run failed: {type(ex).__name__} {err}"[:300]}
+    return {"value": d["elements"] / d["per_step_s"], "unit": "element-steps/s", "cores": d["workers"],
+            "kind": "reference", "sample": f"fedheat (numba, unmodified, baseline/_ref) ExplicitEngine.run on a "
+            f"{divisions}^3 hex cube ({d['elements']} elements), TD cfg2 laws, {steps} steps after a 2-step warm-up "
+            f"(timings per_step_s); the full cfg4 needs n_chunks x V x 8 B = 556 GB of reference chunk buffers"}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    div = args.cpu_sample_div or {"cfg4": 96, "cfg3": 40, "cfg1": 20, "cfg2": 20, "cfg5": 4}[args.config]
-    # warm-up steps inside cpu_oracle_rate: 1 + W, then K timed steps
-    times, elem, threads = cpu_oracle_rate(args.config, div, args.warmup + args.steps, per_step=True)
+    # the FULL workload of the fast arm (same mesh, boundary, extensions and dt),
+    # one oracle step per bench step on all host threads
+    prob = make_problem(args.config, args.divisions, args.precision)
+    t0 = time.perf_counter()
+    ora, dt, threads = oracle_for(prob)
+    setup = time.perf_counter() - t0
+    times = oracle_step_times(ora, dt, args.warmup + args.steps)
     per_step = times[args.warmup:]
     tot = sum(per_step)
+    elem = prob.mesh.n_elements
     value = elem * len(per_step) / tot
-    size = f"grid / {div}" if args.config == "cfg5" else f"{div}^3 cells"
-    sample = (f"{args.config}-family mesh at {size} ({elem} elements; the full workload is sampled "
-              f"per element), one oracle step (oracle/fh_oracle.c, reference op order, OpenMP) per bench step")
+    sample = (f"full {args.config} workload ({elem} elements, the fast arm's mesh, boundary, sources and dt), one "
+              f"oracle step (oracle/fh_oracle.c: the reference's operation order restated in C, fp64, OpenMP on "
+              f"{threads} threads of {cpu_model()}) per bench step")
     line = {
         "impl": "reference", "metric": "element-steps/sec", "value": value, "unit": "element-steps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(per_step),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "sample_divisions": div, "elements_sampled": elem},
+        "config": {"workload": args.config, "elements": elem, "nodes": prob.mesh.n_nodes,
+                   "same_config": args.divisions == 0,
+                   "dt_s": dt, "oracle_setup_s": setup, "cpu": cpu_model()},
         "cpu_baseline": {"value": value, "unit": "element-steps/s", "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "element-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if args.config == "cfg4" and args.numba_divisions > 0:
+        line["reference_numba"] = numba_reference_rate(args.numba_divisions, 3)
     print(json.dumps(line), flush=True)
 
 
@@ -217,6 +288,11 @@ def main():
         eng = make_engine(mesh, prob.material, prob.boundary, rank=rank, world=world, device=local,
                           n_domains=8, slab_axis=2 if prob.name == "cfg4" else -1, part_nodes=args.part_nodes,
                           **prob.engine_kwargs())
+    elif prob.name in ("cfg1", "cfg2") and prob.precision == 64:
+        # small fp64 configs: the reference-exact EXACT engine, whose resident
+        # kernel runs the whole step loop in one cooperative launch
+        eng = fh.ExplicitEngine(mesh, prob.material, prob.boundary, assembly="exact", device=local,
+                                **prob.engine_kwargs())
     else:  # same tiles as the multi-GPU runs: one engine owning all 8 domains
         eng = fh.ExplicitEngine(mesh, prob.material, prob.boundary, assembly="tiled", device=local,
                                 part_nodes=args.part_nodes, n_domains=8,
@@ -224,10 +300,7 @@ def main():
     t_setup = time.perf_counter() - t_setup
     dt = 0.9 * eng.critical_dt(37.0)
     if prob.name == "cfg4":  # moving source: traverse the seeded segment over the run
-        a, b = (np.asarray(v) for v in prob.notes["path"])
-        src = fh.GaussianSource(amp=5.0e6, sigma=0.005, x0=tuple(a), vel=tuple((b - a) / (prob.steps * dt)),
-                                t0=0.0)
-        eng.set_sources([src])
+        eng.set_sources(run_sources(prob, dt))
     st = eng.initial_state(37.0)
     import ctypes as C
 
@@ -236,20 +309,28 @@ def main():
     N.check(L.fh_set_temperature(h, N.ptr(T), T.size, 0, 0.0))
     stream = torch.cuda.ExternalStream(eng.stream())
     rep = N.FhReport()
-    N.check(L.fh_step(h, args.warmup, dt, C.byref(rep)))
-    torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
+    # warm-up right before the timed region (no idle gap for the clocks to drop)
+    N.check(L.fh_step(h, args.warmup, dt, C.byref(rep)))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     L2_BYTES = 126 * 2**20
     flush_l2 = eng.layout()["step_bytes"] < 2 * L2_BYTES
+    resident = eng.layout()["kernels_per_step"] == 0
     wall0 = time.time()
     elapsed = C.c_float(0.0)
-    if not flush_l2:
+    if resident:
+        # the resident EXACT kernel: the K steps are one cooperative launch
+        # (the step loop of solver.py:468-493 on the device); L2 is flushed
+        # (2x-L2 buffer overwritten) right before it
+        scratch = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=f"cuda:{local}")
+        scratch.fill_(1)
+        rc = L.fh_step_timed(h, args.steps, dt, C.byref(rep), C.byref(elapsed))
+    elif not flush_l2:
         # CUDA events recorded on the engine's launch stream around the K launches
         rc = L.fh_step_timed(h, args.steps, dt, C.byref(rep), C.byref(elapsed))
     else:
@@ -319,22 +400,28 @@ def main():
             traffic = json.load(f).get(args.config)
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1:
-        div = args.cpu_sample_div or {"cfg4": 96, "cfg3": 40, "cfg1": 20, "cfg2": 20, "cfg5": 4}[args.config]
-        rate, el, elem, threads = cpu_oracle_rate(args.config, div, 3)
-        cpu = {"value": rate, "unit": "element-steps/s", "cores": threads, "kind": "port",
-               "sample": f"oracle (fh_oracle.c, fp64, reference op order) on the {args.config} family at "
-                         f"{'grid / ' + str(div) if args.config == 'cfg5' else str(div) + '^3 cells'} "
-                         f"({elem} elements), 3 steps after 1 warm-up"}
+        # bounded sample: the oracle on the same full mesh, 1 warm-up + n steps
+        ora, odt, threads = oracle_for(prob)
+        n = 3 if E > 1e6 else 50
+        ts = oracle_step_times(ora, odt, 1 + n)[1:]
+        del ora
+        cpu = {"value": E * n / sum(ts), "unit": "element-steps/s", "cores": threads, "kind": "port",
+               "sample": f"oracle (fh_oracle.c, fp64, reference op order, OpenMP, {cpu_model()}) on the full "
+                         f"{args.config} mesh ({E} elements), {n} steps after 1 warm-up"}
     line = {
         "metric": "element-steps/sec", "value": value, "unit": "element-steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32" if prob.precision == 32 else "f64",
         "data": "synthetic (seeded, BASELINE.json shapes)",
         "config": {"workload": prob.name, "elements": E, "nodes": mesh.n_nodes, "td": prob.td_mode,
-                   "assembly": "tiled", "parts": lay["n_parts"], "slots": lay["n_slots"],
+                   "assembly": "exact (resident: %d steps per launch, %d CTAs)" % (args.steps, lay["resident_ctas"])
+                   if resident else "tiled", "parts": lay["n_parts"], "slots": lay["n_slots"],
                    "parallelism": f"{world} GPU domain decomposition (8 z-slab domains, NCCL halo exchange)"
                    if world > 1 else "1 GPU",
-                   "l2": ("working set < 2x L2: 252 MB buffer overwritten before every timed step" if flush_l2
+                   "l2": ("working set < 2x L2: 252 MB buffer overwritten before the timed launch (the K steps "
+                          "run in one launch; between steps the mesh stays L2/shared-memory resident by design)"
+                          if resident else
+                          "working set < 2x L2: 252 MB buffer overwritten before every timed step" if flush_l2
                           else "per-step input > 2x 126 MB L2 (no flush needed)"), "dt_s": dt, "setup_s": t_setup},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_kind": peak_kind,
@@ -343,7 +430,8 @@ def main():
         "e2e": {"value": E / e2e_s, "unit": "element-steps/s", "h2d_bytes_per_step": 8 * mesh.n_nodes,
                 "d2h_bytes_per_step": 8 * mesh.n_nodes},
         # step kernel launches (one per tile kind and launch range) + halo pack / unpack (N > 1)
-        "gpu_launches": args.steps * (lay["kernels_per_step"] + (2 if world > 1 else 0)),
+        # (resident: one launch for all K steps)
+        "gpu_launches": 1 if resident else args.steps * (lay["kernels_per_step"] + (2 if world > 1 else 0)),
         "clocks": clocks,
     }
     if rank == 0:

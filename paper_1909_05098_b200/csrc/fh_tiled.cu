@@ -38,6 +38,8 @@ constexpr int kMinBlocksF32 = FH_MIN_BLOCKS_F32;
 #define FH_MIN_BLOCKS_TET 5
 #endif
 constexpr int kMinBlocksTet = FH_MIN_BLOCKS_TET;  // tet-only fp32 kernels: smaller tiles, more CTAs
+// tet-only fp64 kernels: 3 resident CTAs (<= 80 registers; cfg3 fp64 runs 4 waves of 3 CTAs/SM)
+constexpr int kMinBlocksTetF64 = 3;
 // global loads kept in flight per thread in the staging and node-update loops
 #ifndef FH_STAGE_UNROLL
 #define FH_STAGE_UNROLL 8
@@ -443,7 +445,8 @@ __device__ __forceinline__ void accumulate_colored(S *acc, const uint16_t (&nd)[
 
 // KINDS: 0 hex-only, 1 tet-only, 2 mixed mesh (the absent kind's path is compiled out)
 template <typename S, bool TD, int MODE, int KINDS, bool LIN>
-__global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? kMinBlocksTet : kMinBlocksF32) : 2)
+__global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? kMinBlocksTet : kMinBlocksF32)
+                                                                : (KINDS == 1 ? kMinBlocksTetF64 : 2))
     k_tiled_step(const __grid_constant__ TiledArgs<S> g) {
   extern __shared__ __align__(128) unsigned char smem[];
   TK<S> *sT = reinterpret_cast<TK<S> *>(smem);

@@ -269,6 +269,22 @@ int fh_nccl_unique_id(char *id128);
  * goes through NCCL): a single-GPU check of the NCCL loading and init path */
 int fh_attach_nccl(fh_engine *e, const char *id128, int32_t rank, int32_t world);
 
+/* Host transport for the multi-GPU halo exchange (instead of NCCL, e.g. over
+ * gloo or MPI on the host).  fh_step then runs the same per-step schedule --
+ * interior tiles, boundary tiles, pack kernel -- copies the packed values to
+ * host memory, calls exchange() (blocking), copies the received values back
+ * and runs the unpack kernel.  Buffers hold elem_bytes-sized values (4 or 8)
+ * grouped by peer, offsets in values (n_peers + 1 entries each).
+ * allreduce_min_u64 replaces *value by the minimum over all ranks (fail-flag
+ * agreement and the instability report).  Callbacks return 0 on success. */
+typedef struct {
+  void *ctx;
+  int32_t (*exchange)(void *ctx, int32_t n_peers, const int32_t *peers, const void *send, const int64_t *send_offs,
+                      void *recv, const int64_t *recv_offs, int32_t elem_bytes);
+  int32_t (*allreduce_min_u64)(void *ctx, uint64_t *value);
+} fh_transport;
+int fh_attach_transport(fh_engine *e, const fh_transport *transport);
+
 /* Halo bookkeeping of a multi-domain engine (rank = domain_lo / width, world =
  * n_domains / width).  Node ids in the original numbering; per-peer ranges
  * [offs[q], offs[q+1]).  fh_halo_export/import move the current halo values

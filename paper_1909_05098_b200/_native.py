@@ -74,6 +74,16 @@ class FhOptions(C.Structure):
     ] + [(name, C.c_int32) for name in TUNING_FIELDS]
 
 
+# fh_transport (host halo exchange instead of NCCL)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_void_p, C.POINTER(C.c_int64),
+                          C.c_void_p, C.POINTER(C.c_int64), C.c_int32)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.POINTER(C.c_uint64))
+
+
+class FhTransport(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("exchange", EXCHANGE_FN), ("allreduce_min_u64", ALLREDUCE_FN)]
+
+
 class FhReport(C.Structure):
     _fields_ = [("steps_done", C.c_int64), ("fail_step", C.c_int64), ("fail_node", C.c_int64),
                 ("fail_value", C.c_double), ("time", C.c_double), ("step_index", C.c_int64)]
@@ -93,7 +103,7 @@ EXPORTS = [
     "fh_set_temperature", "fh_get_temperature", "fh_get_inflow", "fh_keep_inflow", "fh_reset_properties", "fh_step",
     "fh_step_timed", "fh_step_timed_flush", "fh_step_host", "fh_step_host_async", "fh_host_wait", "fh_set_q_static", "fh_set_sources", "fh_set_probes", "fh_get_probes", "fh_critical_dt", "fh_scatter_loads",
     "fh_get_precompute", "fh_get_layout", "fh_stream", "fh_get_node_order", "fh_nccl_unique_id",
-    "fh_attach_nccl", "fh_halo_info", "fh_halo_lists", "fh_halo_export", "fh_halo_import", "fh_get_owned",
+    "fh_attach_nccl", "fh_attach_transport", "fh_halo_info", "fh_halo_lists", "fh_halo_export", "fh_halo_import", "fh_get_owned",
     "fh_plan_create", "fh_plan_info", "fh_plan_arrays", "fh_plan_destroy", "fh_mesh_parse", "fh_mesh_text_info",
     "fh_mesh_text_arrays", "fh_mesh_text_set", "fh_mesh_text_destroy", "fh_format_f64", "fh_format_i64",
 ]
@@ -144,6 +154,7 @@ def lib():
     L.fh_nodal_update.argtypes = [f64p, f64p, f64p, f64p, f64p, f64p, f64p, C.c_int64, C.c_double]
     L.fh_nccl_unique_id.argtypes = [C.c_char_p]
     L.fh_attach_nccl.argtypes = [C.c_void_p, C.c_char_p, C.c_int32, C.c_int32]
+    L.fh_attach_transport.argtypes = [C.c_void_p, C.POINTER(FhTransport)]
     i32o = C.POINTER(C.c_int32)
     L.fh_halo_info.argtypes = [C.c_void_p, i32o, i32o, i32o, i64p, i64p, i64p, i64p]
     L.fh_halo_lists.argtypes = [C.c_void_p, i32p, i64p, i64p, i64p, i64p]

@@ -115,7 +115,9 @@ template <typename S>
 __global__ void k_to_old(const S *__restrict__ src_new, const int64_t *__restrict__ new_of_old, int64_t V,
                          double *__restrict__ dst_old) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < V) dst_old[i] = (double)src_new[new_of_old ? new_of_old[i] : i];
+  if (i >= V) return;
+  const int64_t n = new_of_old ? new_of_old[i] : i;
+  dst_old[i] = n >= 0 ? (double)src_new[n] : __longlong_as_double(0x7ff8000000000000ll);  // not in this rank's view
 }
 
 template <typename S>
@@ -186,6 +188,7 @@ struct fh_engine {
   int precision = 64, assembly = FH_ASSEMBLY_EXACT;
   bool td = false;
   int64_t V = 0, E = 0, n_tet = 0, n_hex = 0, nconn = 0;
+  int64_t Vt = 0;  // TILED: nodes of the device node arrays (V, or the rank's owned + halo nodes)
   double runaway_limit = 1e6;
   bool dir_runaway = false;  // some |Dirichlet value| > runaway_limit: every step fails
   bool keep_inflow = false;  // TILED: the step kernel also writes F (fh_keep_inflow)
@@ -241,6 +244,10 @@ struct fh_engine {
   cudaEvent_t ev_packed = nullptr, ev_halo = nullptr;
   bool halo_pending = false;
   void *comm = nullptr;  // ncclComm_t
+  fh_transport transport{};  // host transport (fh_attach_transport), instead of NCCL
+  DBuf<unsigned long long> red_scratch;  // NCCL all-reduce of host values
+  std::vector<char> x_host_send, x_host_recv;
+  DBuf<char> snap;  // multi-GPU: the field at the start of an fh_step call (exact failure replay)
   // probes
   DBuf<int32_t> probes;
   int64_t n_probes = 0, probe_interval = 1, probe_cap = 0, n_rec = 0;
@@ -396,9 +403,9 @@ void upload_qr(fh_engine *e, double t) {
     for (int64_t i = 0; i < e->V; ++i) qr[i] += e->q_static[i];
   FH_CUDA(cudaMemcpy(e->stage.p, qr.data(), sizeof(double) * e->V, cudaMemcpyHostToDevice));
   if (e->precision == 32)
-    k_to_new<<<nblk(e->V), kBlk>>>(e->stage.p, e->old_of_new.p, e->V, e->tf->q_ext.p, nullptr, nullptr, nullptr);
+    k_to_new<<<nblk(e->Vt), kBlk>>>(e->stage.p, e->old_of_new.p, e->Vt, e->tf->q_ext.p, nullptr, nullptr, nullptr);
   else
-    k_to_new<<<nblk(e->V), kBlk>>>(e->stage.p, e->old_of_new.p, e->V, nullptr, e->tdd->q_ext.p, nullptr, nullptr);
+    k_to_new<<<nblk(e->Vt), kBlk>>>(e->stage.p, e->old_of_new.p, e->Vt, nullptr, e->tdd->q_ext.p, nullptr, nullptr);
   FH_CUDA(cudaGetLastError());
   FH_CUDA(cudaDeviceSynchronize());
 }
@@ -581,8 +588,6 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   pin.slab_axis = o.slab_axis;
   build_partition(pin, e->part);
   Partition &P = e->part;
-  e->old_of_new.upload(P.old_of_new, s);
-  e->new_of_old.upload(P.new_of_old, s);
 
   auto st = std::make_unique<TiledState<S>>();
   TiledArgs<S> &g = st->args;
@@ -598,6 +603,18 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     for (int64_t i : e->dir_nodes) is_dir[P.new_of_old[i]] = 1;
     build_exchange(P, is_dir.data(), D, D / width, dlo / width, e->X);
   }
+  // multi-GPU: keep only this rank's parts, slots and the nodes they read
+  // (local numbering: owned range, then the foreign halo nodes), so the
+  // per-step device working set is the rank's share of the mesh
+  if (e->X.world > 1) {
+    Partition Lp;
+    localize_partition(P, e->X, Lp);
+    P = std::move(Lp);
+  }
+  const int64_t Vt = (int64_t)P.old_of_new.size();  // nodes of the tiled arrays (V on one GPU)
+  e->Vt = Vt;
+  e->old_of_new.upload(P.old_of_new, s);
+  e->new_of_old.upload(P.new_of_old, s);
   std::vector<int32_t> plist = e->X.part_order;  // boundary tiles first
   st->n_parts_local = (int)plist.size();
   st->n_boundary = e->X.world > 1 ? e->X.n_boundary : 0;
@@ -746,22 +763,22 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
                                                kBatch * 8 * 2 / (int)sizeof(S), e->kfactor.p, st->hex_kf.p,
                                                e->elem_region.p, st->hex_region.p);
   FH_CUDA(cudaGetLastError());
-  // nodal arrays in the new numbering
-  st->T[0].alloc(V);
-  st->T[1].alloc(V);
-  st->vol.alloc(V);
+  // nodal arrays in the new (multi-GPU: rank-local) numbering
+  st->T[0].alloc(Vt);
+  st->T[1].alloc(Vt);
+  st->vol.alloc(Vt);
   {
     float *vf = nullptr;
     double *vd = nullptr;
     if constexpr (sizeof(S) == 4) vf = st->vol.p; else vd = st->vol.p;
-    k_to_new<<<nblk(V), kBlk, 0, s>>>(e->node_vol.p, e->old_of_new.p, V, vf, vd, nullptr, nullptr);
+    k_to_new<<<nblk(Vt), kBlk, 0, s>>>(e->node_vol.p, e->old_of_new.p, Vt, vf, vd, nullptr, nullptr);
   }
   if (regions) {
     std::vector<int32_t> nr(V);
     FH_CUDA(cudaMemcpyAsync(nr.data(), e->node_region.p, sizeof(int32_t) * V, cudaMemcpyDeviceToHost, s));
     FH_CUDA(cudaStreamSynchronize(s));
-    std::vector<uint8_t> nrn(V);
-    for (int64_t n = 0; n < V; ++n) nrn[n] = (uint8_t)nr[P.old_of_new[n]];
+    std::vector<uint8_t> nrn(Vt);
+    for (int64_t n = 0; n < Vt; ++n) nrn[n] = (uint8_t)nr[P.old_of_new[n]];
     st->node_region.upload(nrn, s);
     // per tile: the material of its updated nodes when they all share one
     // (the node update then reads the laws as uniform operands), else -1
@@ -776,24 +793,24 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     st->part_mat.upload(pm, s);
   }
   if (!e->td) {
-    st->cap.alloc(V);
-    st->kb.alloc(V);
+    st->cap.alloc(Vt);
+    st->kb.alloc(Vt);
     st->tet_kbar.alloc(nts);
     st->hex_kbar.alloc(nhs);
   }
   if (!e->q_static.empty() || !e->load_power.empty()) {
-    st->q_ext.alloc(V);
+    st->q_ext.alloc(Vt);
     if (e->load_power.empty()) {
       FH_CUDA(cudaMemcpyAsync(e->stage.p, e->q_static.data(), sizeof(double) * V, cudaMemcpyHostToDevice, s));
       float *qf = nullptr;
       double *qd = nullptr;
       if constexpr (sizeof(S) == 4) qf = st->q_ext.p; else qd = st->q_ext.p;
-      k_to_new<<<nblk(V), kBlk, 0, s>>>(e->stage.p, e->old_of_new.p, V, qf, qd, nullptr, nullptr);
+      k_to_new<<<nblk(Vt), kBlk, 0, s>>>(e->stage.p, e->old_of_new.p, Vt, qf, qd, nullptr, nullptr);
     }
   }
   if (!e->sources.empty()) {
-    st->xyz.alloc(4 * V);
-    k_xyzv_to_new<S><<<nblk(V), kBlk, 0, s>>>(e->xyz.p, e->old_of_new.p, st->vol.p, V, st->xyz.p);
+    st->xyz.alloc(4 * Vt);
+    k_xyzv_to_new<S><<<nblk(Vt), kBlk, 0, s>>>(e->xyz.p, e->old_of_new.p, st->vol.p, Vt, st->xyz.p);
     FH_CUDA(cudaGetLastError());
   }
   if (!e->robin_nodes.empty()) {
@@ -811,11 +828,13 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     st->robin_hAT.upload(hat, s);
   }
   if (!e->dir_nodes.empty()) {  // imposed on the device whenever a field is set (solver.py:364-365)
-    std::vector<int32_t> ids(e->dir_nodes.size());
-    std::vector<S> vals(e->dir_nodes.size());
+    std::vector<int32_t> ids;
+    std::vector<S> vals;
     for (size_t q = 0; q < e->dir_nodes.size(); ++q) {
-      ids[q] = (int32_t)P.new_of_old[e->dir_nodes[q]];
-      vals[q] = (S)e->dir_vals[q];
+      const int64_t l = P.new_of_old[e->dir_nodes[q]];
+      if (l < 0) continue;  // not in this rank's view
+      ids.push_back((int32_t)l);
+      vals.push_back((S)e->dir_vals[q]);
     }
     st->dir_ids.upload(ids, s);
     st->dir_vals.upload(vals, s);
@@ -922,7 +941,7 @@ void tiled_set_T(fh_engine *e, const double *src = nullptr) {  // src (default e
     d0 = st.T[0].p;
     d1 = st.T[1].p;
   }
-  k_to_new<<<nblk(e->V), kBlk, 0, e->stream>>>(src ? src : e->stage.p, e->old_of_new.p, e->V, f0, d0, f1, d1);
+  k_to_new<<<nblk(e->Vt), kBlk, 0, e->stream>>>(src ? src : e->stage.p, e->old_of_new.p, e->Vt, f0, d0, f1, d1);
   // the reference steps from the state as given and imposes the Dirichlet
   // values after the update (solver.py:364-365): the first step reads T[0]
   // as set and writes T[1], which already holds the Dirichlet values (the
@@ -966,7 +985,7 @@ void tiled_run(fh_engine *e, int64_t nsteps, double dt) {
     g.Tout = st.T[st.cur ^ 1].p;
     if (!e->td && !e->frozen) {
       const int64_t nts = (int64_t)e->part.tet_slot_elem.size(), nhs = (int64_t)e->part.hex_slot_elem.size();
-      tiled_freeze<S>(g, st.tet_conn.p, st.hex_conn.p, nts, nhs, e->V, st.tet_kf.p, st.hex_kf.p, st.tet_kbar.p, st.hex_kbar.p, st.cap.p,
+      tiled_freeze<S>(g, st.tet_conn.p, st.hex_conn.p, nts, nhs, e->Vt, st.tet_kf.p, st.hex_kf.p, st.tet_kbar.p, st.hex_kbar.p, st.cap.p,
                       st.kb.p, e->stream);
       g.tet_kf = st.tet_kbar.p;
       g.hex_kf = st.hex_kbar.p;
@@ -1041,6 +1060,21 @@ void tiled_run(fh_engine *e, int64_t nsteps, double dt) {
         halo_unpack<S>(g.Tout, e->x_recv.p, (int64_t)e->X.recv_nodes.size(), recvbuf, e->comm_stream);
         FH_CUDA(cudaEventRecord(e->ev_halo, e->comm_stream));
         e->halo_pending = true;
+      } else if (e->transport.exchange) {  // host transport: the same order, blocking exchange on the host
+        S *sendbuf = reinterpret_cast<S *>(e->x_sendbuf.p);
+        S *recvbuf = reinterpret_cast<S *>(e->x_recvbuf.p);
+        const int64_t ns = (int64_t)e->X.send_nodes.size(), nr = (int64_t)e->X.recv_nodes.size();
+        halo_pack<S>(g.Tout, e->x_send.p, ns, sendbuf, e->stream);
+        e->x_host_send.resize(sizeof(S) * std::max<int64_t>(1, ns));
+        e->x_host_recv.resize(sizeof(S) * std::max<int64_t>(1, nr));
+        FH_CUDA(cudaMemcpyAsync(e->x_host_send.data(), sendbuf, sizeof(S) * ns, cudaMemcpyDeviceToHost, e->stream));
+        FH_CUDA(cudaStreamSynchronize(e->stream));
+        if (e->transport.exchange(e->transport.ctx, (int32_t)e->X.peers.size(), e->X.peers.data(),
+                                  e->x_host_send.data(), e->X.send_offs.data(), e->x_host_recv.data(),
+                                  e->X.recv_offs.data(), (int32_t)sizeof(S)) != 0)
+          fail(FH_ERR_DEVICE, "host transport exchange failed");
+        FH_CUDA(cudaMemcpyAsync(recvbuf, e->x_host_recv.data(), sizeof(S) * nr, cudaMemcpyHostToDevice, e->stream));
+        halo_unpack<S>(g.Tout, e->x_recv.p, nr, recvbuf, e->stream);
       }
     }
     if (e->dir_runaway) k_flag_step<<<1, 1, 0, e->stream>>>(e->flag.p, g.step_no);
@@ -1147,6 +1181,88 @@ void run_steps(fh_engine *e, int64_t nsteps, double dt) {
     tiled_run<double>(e, nsteps, dt);
 }
 
+// min over ranks of a host value (NCCL or the host transport; world 1: as is)
+void rank_min_u64(fh_engine *e, unsigned long long &v) {
+  if (e->comm) {
+    if (!e->red_scratch.p) e->red_scratch.alloc(1);
+    FH_CUDA(cudaMemcpyAsync(e->red_scratch.p, &v, sizeof(v), cudaMemcpyHostToDevice, e->stream));
+    nccl_min_u64(e->comm, e->red_scratch.p, e->stream);
+    FH_CUDA(cudaMemcpyAsync(&v, e->red_scratch.p, sizeof(v), cudaMemcpyDeviceToHost, e->stream));
+    FH_CUDA(cudaStreamSynchronize(e->stream));
+  } else if (e->transport.allreduce_min_u64) {
+    uint64_t x = v;
+    if (e->transport.allreduce_min_u64(e->transport.ctx, &x) != 0) fail(FH_ERR_DEVICE, "host transport all-reduce failed");
+    v = x;
+  }
+}
+
+bool multi_rank(const fh_engine *e) {
+  return e->assembly != FH_ASSEMBLY_EXACT && e->X.world > 1 && (e->comm || e->transport.exchange);
+}
+
+// the field the next step reads, copied to / from e->snap (multi-GPU replay)
+template <typename S>
+void snapshot_T(fh_engine *e, bool restore) {
+  TiledState<S> &st = tstate<S>(e);
+  const size_t bytes = sizeof(S) * (size_t)e->Vt;
+  if (!e->snap.p) e->snap.alloc(bytes);
+  if (restore)
+    FH_CUDA(cudaMemcpyAsync(st.T[st.cur].p, e->snap.p, bytes, cudaMemcpyDeviceToDevice, e->stream));
+  else
+    FH_CUDA(cudaMemcpyAsync(e->snap.p, st.T[st.cur].p, bytes, cudaMemcpyDeviceToDevice, e->stream));
+}
+
+// The instability report's node (solver.py:369-382: first non-finite node,
+// else the first node of largest |T|) over this rank's owned nodes, agreed
+// across ranks; returns the node (original id) and its value.
+int64_t failure_node(fh_engine *e, double &value) {
+  current_T_to_stage(e);
+  std::vector<double> T(e->V);
+  FH_CUDA(cudaMemcpyAsync(T.data(), e->stage.p, sizeof(double) * e->V, cudaMemcpyDeviceToHost, e->stream));
+  FH_CUDA(cudaStreamSynchronize(e->stream));
+  const bool multi = multi_rank(e);
+  std::vector<int64_t> owned;  // original ids of the owned nodes, ascending
+  if (multi) {
+    owned.assign(e->part.old_of_new.begin() + e->X.node_lo, e->part.old_of_new.begin() + e->X.node_hi);
+    std::sort(owned.begin(), owned.end());
+  }
+  const int64_t n_scan = multi ? (int64_t)owned.size() : e->V;
+  auto id = [&](int64_t k) { return multi ? owned[k] : k; };
+  const unsigned long long none = ~0ull;
+  unsigned long long nf = none;
+  for (int64_t k = 0; k < n_scan; ++k)
+    if (!std::isfinite(T[id(k)])) {
+      nf = (unsigned long long)id(k);
+      break;
+    }
+  rank_min_u64(e, nf);
+  int64_t node;
+  if (nf != none) {
+    node = (int64_t)nf;
+  } else {
+    double best = -1.0;
+    int64_t arg = -1;
+    for (int64_t k = 0; k < n_scan; ++k)
+      if (std::fabs(T[id(k)]) > best) {
+        best = std::fabs(T[id(k)]);
+        arg = id(k);
+      }
+    // max |T| over ranks (non-negative doubles order like their bits), then
+    // the lowest node id attaining it
+    unsigned long long nb = ~(arg >= 0 ? (unsigned long long)__builtin_bit_cast(uint64_t, best) : 0ull);
+    rank_min_u64(e, nb);
+    unsigned long long cand = (arg >= 0 && ~nb == __builtin_bit_cast(uint64_t, best)) ? (unsigned long long)arg : none;
+    rank_min_u64(e, cand);
+    node = (int64_t)cand;
+  }
+  // the owning rank supplies the value
+  bool mine = !multi || std::binary_search(owned.begin(), owned.end(), node);
+  unsigned long long vb = mine ? __builtin_bit_cast(uint64_t, T[node]) : none;
+  if (multi) rank_min_u64(e, vb);
+  value = __builtin_bit_cast(double, (uint64_t)vb);
+  return node;
+}
+
 int do_step(fh_engine *e, int64_t nsteps, double dt, fh_report *rep, float *elapsed_ms = nullptr,
             void *scratch = nullptr, size_t scratch_bytes = 0) {
   if (nsteps < 0) fail(FH_ERR_CONFIG, "nsteps must be >= 0");
@@ -1159,6 +1275,23 @@ int do_step(fh_engine *e, int64_t nsteps, double dt, fh_report *rep, float *elap
     FH_CUDA(cudaEventCreate(&ev[0]));
     FH_CUDA(cudaEventCreate(&ev[1]));
     FH_CUDA(cudaEventRecord(ev[0], e->stream));
+  }
+  // multi-GPU: ranks that did not fail keep stepping until the call ends (the
+  // flag is agreed once per call), so a failure is replayed from the field at
+  // the start of the call for exactly the steps up to the failing one
+  const bool multi = multi_rank(e);
+  const int64_t nrec0 = e->n_rec;
+  const size_t nps0 = e->probe_steps.size();
+  const double time0 = e->time;
+  bool dir_pending0 = false;
+  if (multi) {
+    if (e->precision == 32) {
+      dir_pending0 = e->tf->dir_pending;
+      snapshot_T<float>(e, false);
+    } else {
+      dir_pending0 = e->tdd->dir_pending;
+      snapshot_T<double>(e, false);
+    }
   }
   if (scratch) {
     sev.resize(2 * nsteps);
@@ -1189,6 +1322,51 @@ int do_step(fh_engine *e, int64_t nsteps, double dt, fh_report *rep, float *elap
   }
   if (e->comm)  // every rank agrees on the first failing step
     nccl_min_u64(e->comm, &e->flag.p->step, e->stream);
+  else if (e->transport.allreduce_min_u64) {
+    FailFlag f0{};
+    FH_CUDA(cudaMemcpyAsync(&f0, e->flag.p, sizeof(f0), cudaMemcpyDeviceToHost, e->stream));
+    FH_CUDA(cudaStreamSynchronize(e->stream));
+    rank_min_u64(e, f0.step);
+    FH_CUDA(cudaMemcpyAsync(e->flag.p, &f0, sizeof(f0), cudaMemcpyHostToDevice, e->stream));
+  }
+  if (multi) {
+    FailFlag fr{};
+    FH_CUDA(cudaMemcpyAsync(&fr, e->flag.p, sizeof(fr), cudaMemcpyDeviceToHost, e->stream));
+    FH_CUDA(cudaStreamSynchronize(e->stream));
+    if (fr.step != ~0ull) {  // replay steps step0+1 .. fs from the snapshot on every rank
+      const int64_t fs = (int64_t)fr.step;
+      const FailFlag clear{~0ull};
+      FH_CUDA(cudaMemcpyAsync(e->flag.p, &clear, sizeof(clear), cudaMemcpyHostToDevice, e->stream));
+      if (e->precision == 32) {
+        e->tf->cur = cur0;
+        e->tf->dir_pending = dir_pending0;
+        snapshot_T<float>(e, true);
+      } else {
+        e->tdd->cur = cur0;
+        e->tdd->dir_pending = dir_pending0;
+        snapshot_T<double>(e, true);
+      }
+      e->step_index = step0;
+      e->time = time0;
+      e->n_rec = nrec0;
+      e->probe_steps.resize(nps0);
+      e->qr_valid = false;
+      run_steps(e, fs - step0, dt);
+      if (e->halo_pending) {
+        FH_CUDA(cudaStreamWaitEvent(e->stream, e->ev_halo, 0));
+        e->halo_pending = false;
+      }
+      // the failing step ran again on its rank: the flag holds fs there
+      if (e->comm) nccl_min_u64(e->comm, &e->flag.p->step, e->stream);
+      else {
+        FailFlag f1{};
+        FH_CUDA(cudaMemcpyAsync(&f1, e->flag.p, sizeof(f1), cudaMemcpyDeviceToHost, e->stream));
+        FH_CUDA(cudaStreamSynchronize(e->stream));
+        rank_min_u64(e, f1.step);
+        FH_CUDA(cudaMemcpyAsync(e->flag.p, &f1, sizeof(f1), cudaMemcpyHostToDevice, e->stream));
+      }
+    }
+  }
   if (elapsed_ms && !scratch) {
     FH_CUDA(cudaEventRecord(ev[1], e->stream));
     FH_CUDA(cudaEventSynchronize(ev[1]));
@@ -1218,28 +1396,12 @@ int do_step(fh_engine *e, int64_t nsteps, double dt, fh_report *rep, float *elap
       e->n_rec--;
     }
     // locate the node like solver.py:369-382 (first non-finite, else argmax |T|)
-    current_T_to_stage(e);
-    std::vector<double> T(e->V);
-    FH_CUDA(cudaMemcpyAsync(T.data(), e->stage.p, sizeof(double) * e->V, cudaMemcpyDeviceToHost, e->stream));
-    FH_CUDA(cudaStreamSynchronize(e->stream));
-    int64_t node = -1;
-    for (int64_t i = 0; i < e->V; ++i)
-      if (!std::isfinite(T[i])) {
-        node = i;
-        break;
-      }
-    if (node < 0) {
-      double best = -1.0;
-      for (int64_t i = 0; i < e->V; ++i)
-        if (std::fabs(T[i]) > best) {
-          best = std::fabs(T[i]);
-          node = i;
-        }
-    }
+    double fail_value = 0.0;
+    const int64_t node = failure_node(e, fail_value);
     if (rep) {
       rep->fail_step = fs;
       rep->fail_node = node;
-      rep->fail_value = T[node];
+      rep->fail_value = fail_value;
       rep->steps_done = fs - step0;
       rep->time = e->time;
       rep->step_index = e->step_index;
@@ -1493,7 +1655,7 @@ int fh_keep_inflow(fh_engine *e, int32_t on) {
   if (e->keep_inflow) {
     auto alloc = [&](auto &st) {
       if (!st.F.p) {
-        st.F.alloc(e->V);
+        st.F.alloc(e->Vt);
         st.F.zero(e->stream);  // Dirichlet nodes are not updated: their entries stay 0
         FH_CUDA(cudaStreamSynchronize(e->stream));
       }
@@ -1669,7 +1831,7 @@ int fh_set_q_static(fh_engine *e, const double *q, int64_t n) {
     auto set = [&](auto &st) {
       using S = std::remove_reference_t<decltype(*st.T[0].p)>;
       if (!st.q_ext.p) {
-        st.q_ext.alloc(e->V);
+        st.q_ext.alloc(e->Vt);
         st.args.q_ext = st.q_ext.p;
       }
       if (e->load_power.empty()) {
@@ -1677,7 +1839,7 @@ int fh_set_q_static(fh_engine *e, const double *q, int64_t n) {
         float *qf = nullptr;
         double *qd = nullptr;
         if constexpr (sizeof(S) == 4) qf = st.q_ext.p; else qd = st.q_ext.p;
-        k_to_new<<<nblk(e->V), kBlk, 0, e->stream>>>(e->stage.p, e->old_of_new.p, e->V, qf, qd, nullptr, nullptr);
+        k_to_new<<<nblk(e->Vt), kBlk, 0, e->stream>>>(e->stage.p, e->old_of_new.p, e->Vt, qf, qd, nullptr, nullptr);
         FH_CUDA(cudaGetLastError());
       } else {
         e->qr_valid = false;  // loads + static power are recombined at the next step
@@ -1701,8 +1863,8 @@ int fh_set_sources(fh_engine *e, const fh_source *sources, int32_t n) {
     auto setup = [&](auto &st) {
       using S = std::remove_reference_t<decltype(*st.T[0].p)>;
       if (n > 0 && !st.xyz.p) {
-        st.xyz.alloc(4 * e->V);
-        k_xyzv_to_new<S><<<nblk(e->V), kBlk, 0, e->stream>>>(e->xyz.p, e->old_of_new.p, st.vol.p, e->V, st.xyz.p);
+        st.xyz.alloc(4 * e->Vt);
+        k_xyzv_to_new<S><<<nblk(e->Vt), kBlk, 0, e->stream>>>(e->xyz.p, e->old_of_new.p, st.vol.p, e->Vt, st.xyz.p);
         FH_CUDA(cudaGetLastError());
         st.args.xyzv = st.xyz.p;
       }
@@ -1720,6 +1882,7 @@ int fh_set_probes(fh_engine *e, const int64_t *nodes, int64_t n, int64_t interva
   std::vector<int32_t> p(n);
   for (int64_t q = 0; q < n; ++q) {
     if (nodes[q] < 0 || nodes[q] >= e->V) fail(FH_ERR_CONFIG, "probe node index out of range");
+    // TILED multi-GPU: -1 for a node outside this rank's view (recorded as NaN)
     p[q] = (int32_t)(e->assembly == FH_ASSEMBLY_EXACT ? nodes[q] : e->part.new_of_old[nodes[q]]);
   }
   e->probes.upload(p, e->stream);
@@ -1749,6 +1912,9 @@ int fh_critical_dt(fh_engine *e, const double *T, int64_t n, double *out) {
   FH_API_BEGIN
   check_engine(e);
   if (T && n != e->V) fail(FH_ERR_CONFIG, "field has the wrong length");
+  if (!T && e->assembly != FH_ASSEMBLY_EXACT && e->X.world > 1)
+    fail(FH_ERR_CONFIG, "a multi-GPU engine holds only its share of the field: pass the gathered field "
+                        "(dist.gather_temperature) to fh_critical_dt");
   if (T)
     FH_CUDA(cudaMemcpyAsync(e->stage.p, T, sizeof(double) * e->V, cudaMemcpyHostToDevice, e->stream));
   else
@@ -1866,10 +2032,13 @@ int fh_get_node_order(fh_engine *e, int64_t *new_to_old, int64_t n) {
   FH_API_BEGIN
   check_engine(e);
   if (n != e->V) fail(FH_ERR_CONFIG, "output has the wrong length");
-  if (e->assembly == FH_ASSEMBLY_EXACT)
+  if (e->assembly == FH_ASSEMBLY_EXACT) {
     for (int64_t i = 0; i < n; ++i) new_to_old[i] = i;
-  else
-    std::memcpy(new_to_old, e->part.old_of_new.data(), sizeof(int64_t) * n);
+  } else {  // multi-GPU: the rank's local order (owned, then halo nodes), then -1
+    const int64_t nl = (int64_t)e->part.old_of_new.size();
+    std::memcpy(new_to_old, e->part.old_of_new.data(), sizeof(int64_t) * nl);
+    for (int64_t i = nl; i < n; ++i) new_to_old[i] = -1;
+  }
   FH_API_END
 }
 
@@ -2007,6 +2176,16 @@ int fh_nccl_unique_id(char *id128) {
   FH_API_END
 }
 
+int fh_attach_transport(fh_engine *e, const fh_transport *t) {
+  FH_API_BEGIN
+  check_engine(e);
+  if (e->assembly != FH_ASSEMBLY_TILED) fail(FH_ERR_CONFIG, "multi-GPU needs TILED mode");
+  if (!t || !t->exchange || !t->allreduce_min_u64) fail(FH_ERR_CONFIG, "transport needs both callbacks");
+  if (e->comm) fail(FH_ERR_CONFIG, "the engine already uses NCCL");
+  e->transport = *t;
+  FH_API_END
+}
+
 int fh_attach_nccl(fh_engine *e, const char *id128, int32_t rank, int32_t world) {
   FH_API_BEGIN
   check_engine(e);
@@ -2113,6 +2292,9 @@ int fh_get_owned(fh_engine *e, uint8_t *mask, int64_t n) {
 struct fh_plan {
   Partition P;
   Exchange X;
+  // the rank's local view (localize_partition): what its engine keeps on the device
+  int64_t rank_slots = 0, rank_real_slots = 0, rank_local_nodes = 0, rank_owned_nodes = 0, rank_step_bytes = 0,
+          rank_device_bytes = 0;
 };
 
 int fh_plan_create(const fh_mesh *mesh, const fh_boundary *bnd, const fh_options *opts, int32_t world, int32_t rank,
@@ -2150,6 +2332,25 @@ int fh_plan_create(const fh_mesh *mesh, const fh_boundary *bnd, const fh_options
   std::vector<uint8_t> is_dir(V, 0);
   for (int64_t q = 0; q < bnd->n_dirichlet; ++q) is_dir[pl->P.new_of_old[bnd->dirichlet_nodes[q]]] = 1;
   build_exchange(pl->P, is_dir.data(), pin.n_domains, world, rank, pl->X);
+  {
+    Exchange Xc = pl->X;
+    Partition L;
+    localize_partition(pl->P, Xc, L);
+    const int64_t sb = opts->precision == 32 ? 4 : 8;
+    const int64_t nts = (int64_t)L.tet_slot_elem.size(), nhs = (int64_t)L.hex_slot_elem.size();
+    int64_t real = 0;
+    for (int p = 0; p < L.n_parts; ++p) real += L.part_tet_count[p] + L.part_hex_count[p];
+    pl->rank_slots = nts + nhs;
+    pl->rank_real_slots = real;
+    pl->rank_local_nodes = (int64_t)L.old_of_new.size();
+    pl->rank_owned_nodes = Xc.node_hi - Xc.node_lo;
+    // per step: slot records (16-bit conn + 6 G) + T read/write and v of the owned nodes + halo T reads
+    const int64_t rec = nts * (8 + 6 * sb) + nhs * (16 + 6 * sb);
+    pl->rank_step_bytes = rec + pl->rank_owned_nodes * 3 * sb + (pl->rank_local_nodes - pl->rank_owned_nodes) * sb;
+    // resident step arrays: records, T[2] and v (local nodes), halo id lists, tile tables
+    pl->rank_device_bytes = rec + pl->rank_local_nodes * 3 * sb + 4 * (int64_t)L.halo_nodes.size() +
+                            4 * 12 * (int64_t)(L.n_parts + 1);
+  }
   *out = pl.release();
   FH_API_END
 }
@@ -2168,7 +2369,8 @@ int fh_plan_info(fh_plan *pl, int64_t *info, int32_t n_info) {
                        (int64_t)(pl->P.tet_slot_elem.size() + pl->P.hex_slot_elem.size()), pl->P.max_local_nodes,
                        (int64_t)pl->P.colored_ok, pl->P.max_colors, pl->P.max_nph_tet, pl->P.max_nph_hex,
                        sum_u8(pl->P.tet_batch_nph), (int64_t)pl->P.tet_batch_nph.size(), sum_u8(pl->P.hex_batch_nph),
-                       (int64_t)pl->P.hex_batch_nph.size()};
+                       (int64_t)pl->P.hex_batch_nph.size(), pl->rank_slots, pl->rank_real_slots, pl->rank_local_nodes,
+                       pl->rank_owned_nodes, pl->rank_step_bytes, pl->rank_device_bytes};
   for (int q = 0; q < n_info && q < (int)(sizeof(v) / sizeof(v[0])); ++q) info[q] = v[q];
   FH_API_END
 }

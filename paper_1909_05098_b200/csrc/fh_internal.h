@@ -165,6 +165,7 @@ struct Partition {
   // built with up to 4 writes per node (row r = the write's rank in its
   // class; stored in bits 14-15 of tet_conn16, local index in bits 0-13)
   int tet_rows = 1;
+  int batch = 256;  // slots per batch the slot ranges are aligned to
 };
 
 void build_partition(const PartitionInput &in, Partition &out);
@@ -184,6 +185,8 @@ struct Exchange {
 };
 void build_exchange(const Partition &P, const uint8_t *is_dirichlet_new, int n_domains, int world, int rank,
                     Exchange &X);
+// rank-local view of P for X's parts (X's lists are rewritten to local ids)
+void localize_partition(const Partition &P, Exchange &X, Partition &L);
 
 // node -> incident conn positions (ascending), positions of the flat
 // tets-then-hexes connectivity (exact order of the reference's conn_data)

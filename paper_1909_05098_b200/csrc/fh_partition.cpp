@@ -24,6 +24,7 @@
 //    node meets every corner index at most once per batch (structured hex
 //    grids) the phase is simply the corner index and no rank bytes are stored.
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -108,6 +109,8 @@ void build_slots(int64_t n_elem, const int64_t *conn_old, int64_t elem_offset, c
 
 void build_partition(const PartitionInput &in, Partition &P) {
   const int64_t V = in.V;
+  P = Partition{};
+  P.batch = in.batch;
   const int target = std::max(64, in.target_part_nodes);
   const int ndom = std::max(1, in.n_domains);
   std::vector<int64_t> idx(V);
@@ -604,6 +607,108 @@ void build_exchange(const Partition &P, const uint8_t *is_dir, int n_domains, in
   X.n_boundary = (int)X.part_order.size();
   for (int p = X.part_lo; p < X.part_hi; ++p)
     if (!boundary[p]) X.part_order.push_back(p);
+}
+
+// Rank-local view (multi-GPU engines): only the rank's parts, their slots and
+// the nodes they read.  Local node ids are the owned range [node_lo, node_hi)
+// shifted to 0, then the foreign nodes the parts' halos reference (sorted by
+// new id: received halo nodes and other ranks' Dirichlet nodes).  Slot and
+// batch arrays are the rank's contiguous slice (part ranges start on batch
+// boundaries).  The exchange lists are mapped to local ids in place.
+void localize_partition(const Partition &P, Exchange &X, Partition &L) {
+  const int p0 = X.part_lo, p1 = X.part_hi, np = p1 - p0;
+  const int64_t node_lo = X.node_lo, n_own = X.node_hi - X.node_lo;
+  std::vector<int32_t> foreign;
+  for (int32_t q = P.part_halo_start[p0]; q < P.part_halo_start[p1]; ++q) {
+    const int32_t n = P.halo_nodes[q];
+    if (n < node_lo || n >= node_lo + n_own) foreign.push_back(n);  // nodes of other ranks' parts
+  }
+  std::sort(foreign.begin(), foreign.end());
+  foreign.erase(std::unique(foreign.begin(), foreign.end()), foreign.end());
+  const int64_t V = (int64_t)P.new_of_old.size();
+  const int64_t n_local = n_own + (int64_t)foreign.size();
+  auto local_of = [&](int64_t n) -> int64_t {
+    if (n >= node_lo && n < node_lo + n_own) return n - node_lo;
+    auto it = std::lower_bound(foreign.begin(), foreign.end(), (int32_t)n);
+    if (it == foreign.end() || *it != n)
+      fail(FH_ERR_DEVICE, "localize_partition: node " + std::to_string(n) + " outside the rank's view [" +
+                              std::to_string(node_lo) + ", +" + std::to_string(n_own) + ")");
+    return n_own + (it - foreign.begin());
+  };
+  L = Partition{};
+  L.n_parts = np;
+  L.new_of_old.assign(V, -1);
+  L.old_of_new.resize(n_local);
+  for (int64_t l = 0; l < n_local; ++l) {
+    const int64_t n = l < n_own ? node_lo + l : foreign[l - n_own];
+    L.old_of_new[l] = P.old_of_new[n];
+    L.new_of_old[P.old_of_new[n]] = l;
+  }
+  auto slice = [](const auto &v, int64_t lo, int64_t hi) { return std::decay_t<decltype(v)>(v.begin() + lo, v.begin() + hi); };
+  L.part_node_start.resize(np + 1);
+  L.part_tet_start.resize(np + 1);
+  L.part_hex_start.resize(np + 1);
+  L.part_halo_start.resize(np + 1);
+  const int32_t ts0 = P.part_tet_start[p0], ts1 = P.part_tet_start[p1];
+  const int32_t hs0 = P.part_hex_start[p0], hs1 = P.part_hex_start[p1];
+  const int32_t h0 = P.part_halo_start[p0];
+  for (int k = 0; k <= np; ++k) {
+    L.part_node_start[k] = (int32_t)(P.part_node_start[p0 + k] - node_lo);
+    L.part_tet_start[k] = P.part_tet_start[p0 + k] - ts0;
+    L.part_hex_start[k] = P.part_hex_start[p0 + k] - hs0;
+    L.part_halo_start[k] = P.part_halo_start[p0 + k] - h0;
+  }
+  L.part_n_free = slice(P.part_n_free, p0, p1);
+  L.part_robin_start = slice(P.part_robin_start, p0, p1);
+  L.part_tet_count = slice(P.part_tet_count, p0, p1);
+  L.part_hex_count = slice(P.part_hex_count, p0, p1);
+  L.part_domain = slice(P.part_domain, p0, p1);
+  L.halo_nodes.resize(P.part_halo_start[p1] - h0);
+  for (size_t q = 0; q < L.halo_nodes.size(); ++q) L.halo_nodes[q] = (int32_t)local_of(P.halo_nodes[h0 + q]);
+  L.tet_conn16 = slice(P.tet_conn16, 4 * (int64_t)ts0, 4 * (int64_t)ts1);
+  L.hex_conn16 = slice(P.hex_conn16, 8 * (int64_t)hs0, 8 * (int64_t)hs1);
+  L.tet_slot_elem = slice(P.tet_slot_elem, ts0, ts1);
+  L.hex_slot_elem = slice(P.hex_slot_elem, hs0, hs1);
+  // per-slot corner ids (padding slots hold node 0: local node 0 then)
+  auto map_conn = [&](const std::vector<int32_t> &c, const std::vector<int32_t> &slot_elem, int N, int64_t s_lo,
+                      int64_t s_hi, std::vector<int32_t> &out) {
+    out.resize(N * (s_hi - s_lo));
+    for (int64_t sl = s_lo; sl < s_hi; ++sl)
+      for (int a = 0; a < N; ++a)
+        out[N * (sl - s_lo) + a] = slot_elem[sl] < 0 ? 0 : (int32_t)local_of(c[N * sl + a]);
+  };
+  if (!P.tet_conn.empty()) map_conn(P.tet_conn, P.tet_slot_elem, 4, ts0, ts1, L.tet_conn);
+  if (!P.hex_conn.empty()) map_conn(P.hex_conn, P.hex_slot_elem, 8, hs0, hs1, L.hex_conn);
+  if (!P.tet_rank.empty()) L.tet_rank = slice(P.tet_rank, 4 * (int64_t)ts0, 4 * (int64_t)ts1);
+  if (!P.hex_rank.empty()) L.hex_rank = slice(P.hex_rank, 8 * (int64_t)hs0, 8 * (int64_t)hs1);
+  if (!P.tet_color.empty()) L.tet_color = slice(P.tet_color, ts0, ts1);
+  if (!P.hex_color.empty()) L.hex_color = slice(P.hex_color, hs0, hs1);
+  if (!P.tet_phase.empty()) L.tet_phase = slice(P.tet_phase, ts0, ts1);
+  if (!P.hex_phase.empty()) L.hex_phase = slice(P.hex_phase, hs0, hs1);
+  if (!P.tet_batch_nph.empty()) L.tet_batch_nph = slice(P.tet_batch_nph, ts0 / P.batch, ts1 / P.batch);
+  if (!P.hex_batch_nph.empty()) L.hex_batch_nph = slice(P.hex_batch_nph, hs0 / P.batch, hs1 / P.batch);
+  L.corner_unique = P.corner_unique;
+  L.max_phase_tet = P.max_phase_tet;
+  L.max_phase_hex = P.max_phase_hex;
+  L.max_part_nodes = P.max_part_nodes;
+  L.max_local_nodes = P.max_local_nodes;
+  L.max_part_free = P.max_part_free;
+  L.colored_ok = P.colored_ok;
+  L.hex_colored = P.hex_colored;
+  L.max_colors = P.max_colors;
+  L.max_nph_tet = P.max_nph_tet;
+  L.max_nph_hex = P.max_nph_hex;
+  L.tet_rows = P.tet_rows;
+  L.batch = P.batch;
+  L.domain_part_start = {0, np};
+  // exchange lists and part order in local terms
+  for (auto &n : X.send_nodes) n = (int32_t)local_of(n);
+  for (auto &n : X.recv_nodes) n = (int32_t)local_of(n);
+  for (auto &p : X.part_order) p -= p0;
+  X.node_lo = 0;
+  X.node_hi = n_own;
+  X.part_lo = 0;
+  X.part_hi = np;
 }
 
 }  // namespace fh

@@ -849,7 +849,7 @@ __global__ void k_probes_t(const S *__restrict__ T, const int32_t *__restrict__ 
                            double *__restrict__ out, const FailFlag *flag) {
   if (flag && flag->step != kNone) return;
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q < np) out[q] = (double)T[probes[q]];
+  if (q < np) out[q] = probes[q] >= 0 ? (double)T[probes[q]] : __longlong_as_double(0x7ff8000000000000ll);
 }
 
 template <typename S>

@@ -38,7 +38,9 @@ class Plan:
 
     INFO = ("n_parts", "rank_parts", "boundary_parts", "n_peers", "n_send", "n_recv", "node_lo", "node_hi",
             "corner_unique", "max_phase_tet", "max_phase_hex", "n_slots", "max_local_nodes", "colored_ok",
-            "max_colors", "max_nph_tet", "max_nph_hex", "sum_nph_tet", "nph_len_tet", "sum_nph_hex", "nph_len_hex")
+            "max_colors", "max_nph_tet", "max_nph_hex", "sum_nph_tet", "nph_len_tet", "sum_nph_hex", "nph_len_hex",
+            "rank_slots", "rank_real_slots", "rank_local_nodes", "rank_owned_nodes", "rank_step_bytes",
+            "rank_device_bytes")
 
     def __init__(self, mesh, material, boundary: BoundarySpec | None = None, *, world: int = 1, rank: int = 0,
                  n_domains: int = DEFAULT_DOMAINS, slab_axis: int = -1, part_nodes: int = 0, precision: int = 32,
@@ -90,12 +92,72 @@ class Plan:
         return self.recv_nodes[self.recv_offs[q]:self.recv_offs[q + 1]]
 
 
+class HostTransport:
+    """fh_transport over torch.distributed point-to-point on host tensors (any
+    backend with send/recv, e.g. gloo): the engine packs its halo on the
+    device, this exchanges the packed values with every peer, the engine
+    unpacks them -- fh_step's NCCL schedule with a blocking host exchange."""
+
+    def __init__(self):
+        self._ex = N.EXCHANGE_FN(self._exchange)
+        self._red = N.ALLREDUCE_FN(self._allreduce)
+        self.struct = N.FhTransport(None, self._ex, self._red)
+        self.error = None
+
+    def _exchange(self, ctx, n_peers, peers, send, send_offs, recv, recv_offs, elem_bytes):
+        try:
+            import torch
+            import torch.distributed as dist
+
+            ct, tt = (C.c_float, torch.float32) if elem_bytes == 4 else (C.c_double, torch.float64)
+            so = [send_offs[q] for q in range(n_peers + 1)]
+            ro = [recv_offs[q] for q in range(n_peers + 1)]
+            sbuf = np.ctypeslib.as_array(C.cast(send, C.POINTER(ct)), shape=(max(so[-1], 1),))
+            rbuf = np.ctypeslib.as_array(C.cast(recv, C.POINTER(ct)), shape=(max(ro[-1], 1),))
+            reqs, outs = [], []
+            for q in range(n_peers):
+                p = int(peers[q])
+                st = torch.from_numpy(sbuf[so[q]:so[q + 1]].copy())
+                rt = torch.empty(ro[q + 1] - ro[q], dtype=tt)
+                reqs += [dist.isend(st, p), dist.irecv(rt, p)]
+                outs.append((q, rt))
+            for r in reqs:
+                r.wait()
+            for q, rt in outs:
+                rbuf[ro[q]:ro[q + 1]] = rt.numpy()
+            return 0
+        except Exception as ex:  # noqa: BLE001 -- reported through the engine's status
+            self.error = ex
+            return 1
+
+    def _allreduce(self, ctx, value):
+        try:
+            import torch
+            import torch.distributed as dist
+
+            # u64 min through an order-preserving shift into int64
+            t = torch.tensor([int(value[0]) - 2**63], dtype=torch.int64)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            value[0] = int(t.item()) + 2**63
+            return 0
+        except Exception as ex:  # noqa: BLE001
+            self.error = ex
+            return 1
+
+
 def make_engine(mesh, material, boundary=None, *, rank: int, world: int, device: int, n_domains=DEFAULT_DOMAINS,
-                slab_axis: int = -1, attach: bool = True, **kwargs) -> ExplicitEngine:
-    """The rank's TILED engine; with ``attach`` the NCCL communicator is set up
-    (rank 0 creates the id, torch.distributed broadcasts it)."""
+                slab_axis: int = -1, attach: bool = True, transport: str = "nccl", **kwargs) -> ExplicitEngine:
+    """The rank's TILED engine (its parts and their nodes only).  With
+    ``attach`` the halo exchange is set up: ``transport="nccl"`` builds the
+    NCCL communicator (rank 0 creates the id, torch.distributed broadcasts
+    it); ``transport="host"`` attaches a HostTransport over the current
+    torch.distributed process group."""
     eng = ExplicitEngine(mesh, material, boundary, assembly="tiled", device=device, n_domains=n_domains,
                          domains=domain_range(rank, world, n_domains), slab_axis=slab_axis, **kwargs)
+    if attach and world > 1 and transport == "host":
+        eng._transport = HostTransport()
+        N.check(N.lib().fh_attach_transport(eng._h, C.byref(eng._transport.struct)))
+        return eng
     if attach and world > 1:
         import torch
         import torch.distributed as dist

@@ -11,6 +11,7 @@
 #include "fh_dist.h"
 #include "fh_tiled.cuh"
 #include "fh_resident.h"
+#include "fh_atomic.h"
 
 using namespace fh;
 
@@ -231,6 +232,11 @@ struct fh_engine {
   DBuf<uint8_t> r_info;
   DBuf<double> T1;
   DBuf<unsigned long long> r_bar;
+  // ATOMIC assembly (fh_atomic.cu): element streams in the TILED numbering
+  AtomicState atom;
+  DBuf<int32_t> a_tet_conn, a_hex_conn;
+  DBuf<char> a_tet_G, a_hex_G, a_F, a_hA, a_hAT;
+  DBuf<uint8_t> a_cls;
   // tiled
   Partition part;
   DBuf<int64_t> old_of_new, new_of_old;
@@ -929,6 +935,72 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     e->tdd = std::move(st);
 }
 
+// ATOMIC: element streams (sorted by smallest new node id), G SoA, node classes
+template <typename S>
+void setup_atomic(fh_engine *e, const fh_mesh &mesh, const double *G_dev) {
+  cudaStream_t s = e->stream;
+  const Partition &P = e->part;
+  auto build = [&](const int64_t *conn, int64_t n, int N, int64_t e0, double scale, DBuf<int32_t> &dconn,
+                   DBuf<char> &dG) {
+    if (n == 0) return;
+    std::vector<int32_t> order(n);
+    std::vector<int64_t> key(n);
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t k = INT64_MAX;
+      for (int a = 0; a < N; ++a) k = std::min<int64_t>(k, P.new_of_old[conn[N * i + a]]);
+      key[i] = k;
+      order[i] = (int32_t)i;
+    }
+    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return key[x] < key[y]; });
+    std::vector<int32_t> c((size_t)N * n), elem(n);
+    for (int64_t i = 0; i < n; ++i) {
+      elem[i] = (int32_t)(e0 + order[i]);
+      for (int a = 0; a < N; ++a) c[(size_t)N * i + a] = (int32_t)P.new_of_old[conn[N * (int64_t)order[i] + a]];
+    }
+    dconn.upload(c, s);
+    DBuf<int32_t> delem;
+    delem.upload(elem, s);
+    dG.alloc(6 * sizeof(S) * (size_t)n);
+    atomic_pack<S>(delem.p, n, G_dev, scale, e->kfactor.p, reinterpret_cast<S *>(dG.p), s);
+    FH_CUDA(cudaStreamSynchronize(s));
+  };
+  build(mesh.tets, e->n_tet, 4, 0, 1.0, e->a_tet_conn, e->a_tet_G);
+  build(mesh.hexes, e->n_hex, 8, e->n_tet, 1.0 / 64.0, e->a_hex_conn, e->a_hex_G);
+  std::vector<uint8_t> cls(e->Vt, 0);
+  for (int p = 0; p < P.n_parts; ++p)
+    for (int32_t n = P.part_node_start[p] + P.part_n_free[p]; n < P.part_node_start[p + 1]; ++n) cls[n] = 2;
+  if (!e->robin_nodes.empty()) {
+    std::vector<S> ha(e->Vt, S(0)), hat(e->Vt, S(0));
+    for (size_t q = 0; q < e->robin_nodes.size(); ++q) {
+      const int64_t n = P.new_of_old[e->robin_nodes[q]];
+      if (n < 0 || cls[n] == 2) continue;  // Dirichlet wins
+      cls[n] = 1;
+      ha[n] = (S)e->robin_hA[q];
+      hat[n] = (S)e->robin_hAT[q];
+    }
+    e->a_hA.alloc(sizeof(S) * (size_t)e->Vt);
+    e->a_hAT.alloc(sizeof(S) * (size_t)e->Vt);
+    FH_CUDA(cudaMemcpyAsync(e->a_hA.p, ha.data(), sizeof(S) * e->Vt, cudaMemcpyHostToDevice, s));
+    FH_CUDA(cudaMemcpyAsync(e->a_hAT.p, hat.data(), sizeof(S) * e->Vt, cudaMemcpyHostToDevice, s));
+    FH_CUDA(cudaStreamSynchronize(s));
+    e->atom.hA = e->a_hA.p;
+    e->atom.hAT = e->a_hAT.p;
+  }
+  e->a_cls.upload(cls, s);
+  e->a_F.alloc(sizeof(S) * (size_t)e->Vt);
+  e->a_F.zero(s);
+  AtomicState &a = e->atom;
+  a.tet_conn = e->a_tet_conn.p;
+  a.hex_conn = e->a_hex_conn.p;
+  a.tet_G = e->a_tet_G.p;
+  a.hex_G = e->a_hex_G.p;
+  a.n_tet = e->n_tet;
+  a.n_hex = e->n_hex;
+  a.V = e->Vt;
+  a.cls = e->a_cls.p;
+  FH_CUDA(cudaStreamSynchronize(s));
+}
+
 template <typename S>
 void tiled_set_T(fh_engine *e, const double *src = nullptr) {  // src (default e->stage): original order
   TiledState<S> &st = tstate<S>(e);
@@ -1039,7 +1111,9 @@ void tiled_run(fh_engine *e, int64_t nsteps, double dt) {
       tiled_step(gh, count - n_mixed, e->td, st.mode, st.smem, e->stream);
       FH_CUDA(cudaStreamWaitEvent(e->stream, e->ev_join, 0));
     };
-    if (e->X.world == 1) {
+    if (e->assembly == FH_ASSEMBLY_ATOMIC) {
+      atomic_step<S>(g, e->atom, reinterpret_cast<S *>(e->a_F.p), e->stream);
+    } else if (e->X.world == 1) {
       launch(0, st.n_parts_local, st.n_mixed_i);
     } else {
       // interior tiles need no halo: they run while the previous step's
@@ -1448,8 +1522,14 @@ int fh_create(const fh_mesh *mesh, const fh_boundary *bnd, const fh_options *opt
   e->td = opts->td_mode != 0;
   e->runaway_limit = opts->runaway_limit;
   if (e->assembly == FH_ASSEMBLY_EXACT && e->precision != 64) fail(FH_ERR_CONFIG, "EXACT mode is fp64 only");
-  if (e->assembly != FH_ASSEMBLY_EXACT && e->assembly != FH_ASSEMBLY_TILED)
+  if (e->assembly != FH_ASSEMBLY_EXACT && e->assembly != FH_ASSEMBLY_TILED && e->assembly != FH_ASSEMBLY_ATOMIC)
     fail(FH_ERR_CONFIG, "unsupported assembly mode");
+  if (e->assembly == FH_ASSEMBLY_ATOMIC) {
+    if (!e->td) fail(FH_ERR_CONFIG, "ATOMIC assembly: temperature-dependent runs only");
+    if (opts->n_materials > 1) fail(FH_ERR_CONFIG, "ATOMIC assembly: one material");
+    if (opts->domain_hi > 0 && opts->domain_hi - std::max(0, opts->domain_lo) < std::max(1, opts->n_domains))
+      fail(FH_ERR_CONFIG, "ATOMIC assembly: single GPU only");
+  }
   e->V = mesh->n_nodes;
   e->n_tet = mesh->n_tets;
   e->n_hex = mesh->n_hexes;
@@ -1548,8 +1628,10 @@ int fh_create(const fh_mesh *mesh, const fh_boundary *bnd, const fh_options *opt
     setup_resident(e.get(), conn, offs, pos);
   } else if (e->precision == 32) {
     setup_tiled<float>(e.get(), *mesh, *bnd, G.p);
+    if (e->assembly == FH_ASSEMBLY_ATOMIC) setup_atomic<float>(e.get(), *mesh, G.p);
   } else {
     setup_tiled<double>(e.get(), *mesh, *bnd, G.p);
+    if (e->assembly == FH_ASSEMBLY_ATOMIC) setup_atomic<double>(e.get(), *mesh, G.p);
   }
   if (e->assembly != FH_ASSEMBLY_EXACT) {  // exact-order critical dt still needs these
     e->ex.V = e->V;
@@ -1996,6 +2078,7 @@ int fh_get_layout(fh_engine *e, fh_layout *out) {
              (st.n_boundary ? (st.n_mixed_b > 0 && st.n_mixed_b < st.n_boundary ? 2 : 1) : 0);
     };
     out->kernels_per_step = e->precision == 32 ? launches(*e->tf) : launches(*e->tdd);
+    if (e->assembly == FH_ASSEMBLY_ATOMIC) out->kernels_per_step = (e->n_tet ? 1 : 0) + (e->n_hex ? 1 : 0) + 1;
     out->n_parts = P.n_parts;
     out->max_part_nodes = P.max_part_nodes;
     const int64_t nts = (int64_t)P.tet_slot_elem.size(), nhs = (int64_t)P.hex_slot_elem.size();

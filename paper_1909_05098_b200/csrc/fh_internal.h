@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include <stdexcept>
 #include <string>
@@ -113,6 +114,24 @@ __device__ __forceinline__ double interp_rn(const Curve<double> &c, double x) {
   while (c.x[j + 1] <= x) ++j;
   return __dadd_rn(__dmul_rn(c.slope[j], __dsub_rn(x, c.x[j])), c.y[j]);
 }
+
+// Device-side bounds checks of the checked build (scripts/build_variant.sh
+// checked "-DFH_CHECKS"; compute-sanitizer is not available on this GPU pool):
+// a failed check prints the site and traps.  Compiled out otherwise.
+#ifdef FH_CHECKS
+#define FH_DEV_CHECK(cond, what)                                                                      \
+  do {                                                                                                \
+    if (!(cond)) {                                                                                    \
+      printf("FH_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x);                                                                       \
+      __trap();                                                                                       \
+    }                                                                                                 \
+  } while (0)
+#else
+#define FH_DEV_CHECK(cond, what) \
+  do {                           \
+  } while (0)
+#endif
 
 struct FailFlag {
   unsigned long long step;  // ~0ull = none

@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(const __grid_consta
   const int n0 = r.cta_node[c], nown = r.cta_node[c + 1] - n0;
   const int h0 = r.cta_halo[c], nh = r.cta_halo[c + 1] - h0, nloc = nown + nh;
   const int q0 = r.cta_inc[c], nq = r.cta_inc[c + 1] - q0;
+  FH_DEV_CHECK(n0 >= 0 && n0 + nown <= g.V && q0 == g.csr_offs[n0], "resident CTA ranges");
 
   // once per launch: the incidences' A rows, local corner nodes, elements and
   // (TI) frozen kbar; the halo ids; the owned nodes' update operands and
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(const __grid_consta
     //    written by other CTAs in the previous step: L2 loads (no stale L1)
     for (int i = tid; i < nloc; i += bd) {
       const int gi = i < nown ? n0 + i : sH[i - nown];
+      FH_DEV_CHECK(gi >= 0 && gi < g.V, "resident staged node");
       const double x = __ldcg(Tc + gi);
       sT[i] = x;
       if (TD && KSTAGE) sK[i] = interp_rn(k0, x);
@@ -134,6 +136,9 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(const __grid_consta
       const int L[8] = {(int)(w.x & 0xffff), (int)(w.x >> 16), (int)(w.y & 0xffff), (int)(w.y >> 16),
                         (int)(w.z & 0xffff), (int)(w.z >> 16), (int)(w.w & 0xffff), (int)(w.w >> 16)};
       const double2 *A2 = reinterpret_cast<const double2 *>(sA + 8 * q);
+#ifdef FH_CHECKS
+      for (int b = 0; b < ((info & 8) ? 8 : 4); ++b) FH_DEV_CHECK(L[b] < nloc, "resident corner outside the staged nodes");
+#endif
       if (info & 8) {
         double Tb[8], A[8];
 #pragma unroll

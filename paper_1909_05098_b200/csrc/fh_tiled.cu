@@ -481,6 +481,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   // The copy is widened to 16-byte boundaries (the list is padded at its end).
   const int h0 = g.part_halo_start[p], nh = g.part_halo_start[p + 1] - h0;
   const int hs = h0 & ~3, hoff = h0 - hs;
+  FH_DEV_CHECK(nn + nh <= g.max_local && nfree <= nn && n0 + nn <= g.n_nodes, "tile node ranges");
   int32_t *s_ids = reinterpret_cast<int32_t *>(acc);
   {
     const uint8_t *bn = (KINDS == 0) ? nullptr : g.tet_bnph;
@@ -539,7 +540,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   for (int base = tid; base < nh; base += U * kTileThreads) {
     int id[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) id[u] = s_ids[hoff + min(base + u * kTileThreads, nh - 1)];
+    for (int u = 0; u < U; ++u) {
+      id[u] = s_ids[hoff + min(base + u * kTileThreads, nh - 1)];
+      FH_DEV_CHECK(id[u] >= 0 && id[u] < g.n_nodes, "halo node id");
+    }
     S x[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) x[u] = __ldg(g.Tin + id[u]);
@@ -593,6 +597,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         const int i = valid[q] ? q * kTileThreads + tid : 0;
         const int reg = t_reg ? (int)stage[Lt.region + i] : tile_reg;
         tet_loads<S, TD, LIN>(g, stage, sT, reg, t_kf, i, nd[q], c[q], rofs[q], t_mask, nfree);
+        FH_DEV_CHECK(nd[q][0] < nn + nh && nd[q][1] < nn + nh && nd[q][2] < nn + nh && nd[q][3] < nn + nh,
+                     "tet corner outside the tile's staged nodes");
         // tets are never corner-unique: colour phases (phase byte per slot) or,
         // if the colouring overflowed, ranked phases (rank byte per corner)
         if (t_col) {
@@ -618,6 +624,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         const int i = valid[q] ? q * kTileThreads + tid : 0;
         const int reg = h_reg ? (int)stage[Lh.region + i] : tile_reg;
         hex_loads<S, TD, LIN>(g, stage, sT, reg, h_kf, i, nd[q], c[q]);
+#ifdef FH_CHECKS
+        for (int a = 0; a < 8; ++a) FH_DEV_CHECK(nd[q][a] < nn + nh, "hex corner outside the tile's staged nodes");
+#endif
         if (MODE == kRanked) {
           const uint2 w = reinterpret_cast<const uint2 *>(stage + Lh.rank)[i];
 #pragma unroll

@@ -64,6 +64,8 @@ struct TiledArgs {
   S dt, runaway_limit;
   FailFlag *flag;
   unsigned long long step_no;
+  int64_t n_nodes;  // length of Tin / Tout (bounds checks of the checked build)
+  int max_local;    // owned + halo nodes a tile may stage (shared-memory capacity)
 };
 
 // one batch record of the connectivity + metric stream in HBM, laid out like

@@ -393,11 +393,11 @@ def main():
         t = torch.tensor([e2e_s], device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    traffic = None
+    traffic = None  # ncu DRAM bytes of this config's step kernel(s) at this precision
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and not resident:
         with open(tpath) as f:
-            traffic = json.load(f).get(args.config)
+            traffic = json.load(f).get(f"{args.config}_f{prob.precision}")
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1:
         # bounded sample: the oracle on the same full mesh, 1 warm-up + n steps

@@ -164,6 +164,8 @@ typedef struct {
   int32_t hex_color;        /* TILED: 0 default, 1 colour-sort hex slots even when corner-unique */
   int32_t first_touch;      /* TILED: 0 default (off), 1 first-touch node order inside tiles */
   int32_t allow_nondeterministic; /* must be 1 for tile_mode = shared-memory atomics (5) */
+  int32_t lean_kernels;     /* TILED: 0 auto (specialised batch loops for tet-only colour / hex-only
+                               two-row corner-phase tiles), 1 off (the general kernel) */
 } fh_options;
 
 typedef struct {

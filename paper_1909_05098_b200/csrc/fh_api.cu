@@ -888,6 +888,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.runaway_limit = (S)e->runaway_limit;
   g.flag = e->flag.p;
   g.n_nodes = Vt;
+  g.lean = o.lean_kernels == 0 ? 1 : 0;
   g.max_local = std::max(1, P.max_local_nodes);
   auto al = [](size_t b) { return (b + 127) & ~(size_t)127; };
   // accumulation mode: corner phases / corner slots need corner-unique tiles;

@@ -443,8 +443,12 @@ __device__ __forceinline__ void accumulate_colored(S *acc, const uint16_t (&nd)[
   }
 }
 
-// KINDS: 0 hex-only, 1 tet-only, 2 mixed mesh (the absent kind's path is compiled out)
-template <typename S, bool TD, int MODE, int KINDS, bool LIN>
+// KINDS: 0 hex-only, 1 tet-only, 2 mixed mesh (the absent kind's path is compiled out).
+// LEAN: the batch loop specialised for the common tiles -- tet-only colour
+// phases or hex-only two-row corner phases, one material, no per-slot kf /
+// region / rank streams, a 2-deep ring -- with every per-batch flag and
+// stage offset a compile-time constant (same arithmetic, same bits).
+template <typename S, bool TD, int MODE, int KINDS, bool LIN, bool LEAN = false>
 __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? kMinBlocksTet : kMinBlocksF32)
                                                                 : (KINDS == 1 ? kMinBlocksTetF64 : 2))
     k_tiled_step(const __grid_constant__ TiledArgs<S> g) {
@@ -574,6 +578,91 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   auto batch_nph = [&](int jj, const uint8_t *bn, int slot0) -> int {
     return jj < kNphCache ? (int)s_nph[jj] : (int)__ldg(bn + slot0 / kBatch);
   };
+  if constexpr (LEAN) {
+    constexpr int N = KINDS == 1 ? 4 : 8;
+    // stage layout without kf / region / rank blocks: conn16 | G | phase (tets)
+    constexpr int kG = kBatch * N * 2, kPhase = kG + 6 * kBatch * (int)sizeof(S);
+    const int sbytes = g.stage_bytes;
+    const uint32_t bar0 = smem_u32(&bars[0]);
+    const int cnt = KINDS == 1 ? t_cnt : h_cnt;
+    for (int j = 0; j < nb; ++j) {
+      const int st = j & 1;
+      unsigned char *stage = ring + st * sbytes;
+      asm volatile(
+          "{\n\t.reg .pred p;\n"
+          "LWAIT_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+          "@!p bra LWAIT_%=;\n}" ::"r"(bar0 + 8u * (uint32_t)st),
+          "r"((uint32_t)(j >> 1) & 1u)
+          : "memory");
+      const bool valid = j * kBatch + tid < cnt;
+      const int i = valid ? tid : 0;  // padding threads read slot 0 (accumulation predicated off)
+      const S *G = reinterpret_cast<const S *>(stage + kG);
+      const S g00 = G[i], g01 = G[kBatch + i], g02 = G[2 * kBatch + i], g11 = G[3 * kBatch + i],
+              g12 = G[4 * kBatch + i], g22 = G[5 * kBatch + i];
+      if constexpr (KINDS == 1) {
+        const uint2 w = reinterpret_cast<const uint2 *>(stage)[i];
+        const uint32_t raw[4] = {w.x & 0xffffu, w.x >> 16, w.y & 0xffffu, w.y >> 16};
+        uint16_t nd[4];
+        int rofs[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          nd[a] = (uint16_t)(raw[a] & t_mask);
+          rofs[a] = (int)(raw[a] >> 14) * nfree;
+        }
+        S T[4], K[4];
+#pragma unroll
+        for (int b2 = 0; b2 < 4; ++b2) {
+          const TK<S> q = sT[nd[b2]];
+          T[b2] = q.t;
+          K[b2] = q.k;
+        }
+        // tet_loads with reg == 0 and kf == 1
+        const S kb = ((K[0] + K[1]) + (K[2] + K[3])) * S(0.25) * S(1);
+        const S d1 = T[1] - T[0], d2 = T[2] - T[0], d3 = T[3] - T[0];
+        S c[4];
+        c[1] = kb * (g00 * d1 + g01 * d2 + g02 * d3);
+        c[2] = kb * (g01 * d1 + g11 * d2 + g12 * d3);
+        c[3] = kb * (g02 * d1 + g12 * d2 + g22 * d3);
+        c[0] = -((c[1] + c[2]) + c[3]);
+        const int ph = stage[kPhase + i];
+        const int nph = j < kNphCache ? (int)s_nph[j] : (int)__ldg(g.tet_bnph + t_start / kBatch + j);
+        accumulate_colored<S, 4>(acc, nd, c, nfree, valid, ph, nph, rofs);
+      } else {
+        const uint4 w = reinterpret_cast<const uint4 *>(stage)[i];
+        uint16_t nd[kSPT][8];
+        nd[0][0] = w.x & 0xffff; nd[0][1] = w.x >> 16; nd[0][2] = w.y & 0xffff; nd[0][3] = w.y >> 16;
+        nd[0][4] = w.z & 0xffff; nd[0][5] = w.z >> 16; nd[0][6] = w.w & 0xffff; nd[0][7] = w.w >> 16;
+        S T[8], K[8];
+#pragma unroll
+        for (int b2 = 0; b2 < 8; ++b2) {
+          const TK<S> q = sT[nd[0][b2]];
+          T[b2] = q.t;
+          K[b2] = q.k;
+        }
+        // hex_loads with reg == 0 and kf == 1
+        const S sum = ((K[0] + K[1]) + (K[2] + K[3])) + ((K[4] + K[5]) + (K[6] + K[7]));
+        const S kb = sum * S(0.125) * S(1);
+        const S gx = ((T[1] - T[0]) + (T[2] - T[3])) + ((T[5] - T[4]) + (T[6] - T[7]));
+        const S gy = ((T[3] - T[0]) + (T[2] - T[1])) + ((T[7] - T[4]) + (T[6] - T[5]));
+        const S gz = ((T[4] - T[0]) + (T[5] - T[1])) + ((T[6] - T[2]) + (T[7] - T[3]));
+        const S u = kb * (g00 * gx + g01 * gy + g02 * gz);
+        const S v = kb * (g01 * gx + g11 * gy + g12 * gz);
+        const S w2 = kb * (g02 * gx + g12 * gy + g22 * gz);
+        const S a0 = u + v, b0 = u - v;
+        S c[kSPT][8];
+        c[0][0] = -a0 - w2; c[0][1] = b0 - w2; c[0][2] = a0 - w2; c[0][3] = -b0 - w2;
+        c[0][4] = -a0 + w2; c[0][5] = b0 + w2; c[0][6] = a0 + w2; c[0][7] = -b0 + w2;
+        const bool vv[kSPT] = {valid};
+        uint8_t rk[kSPT][8];
+        accumulate<S, 8, MODE>(acc, nd, c, nfree, vv, rk, 0);
+      }
+      if (tid == 0 && j + 2 < nb) {
+        fence_proxy_async();
+        issue_batch(g, p, j + 2, nbt, stage, &bars[st], false);
+      }
+    }
+  } else {
   int st = 0;
   uint32_t parity = 0;
   for (int j = 0; j < nb; ++j) {
@@ -659,6 +748,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       parity ^= 1u;
     }
   }
+  }  // generic batch loop
   __syncthreads();
 
   // lumped nodal update of the owned free nodes.  The per-tile uniform
@@ -785,9 +875,20 @@ void (*pick_step_kernel(const TiledArgs<S> &g, bool td, int mode_sel, size_t sme
   const int mode = mode_sel < 0 || mode_sel > 6 ? 0 : mode_sel;
   const int kinds = (g.tet_rec && g.hex_rec) ? 2 : (g.hex_rec ? 0 : 1);
   const int lin = g.lin ? 1 : 0;
-  const K kern = table[lin][td ? 1 : 0][kinds][mode];
-  static size_t configured[2][2][3][7] = {};
-  size_t &cfg = configured[lin][td ? 1 : 0][kinds][mode];
+  K kern = table[lin][td ? 1 : 0][kinds][mode];
+  // the LEAN batch loops (see k_tiled_step)
+  const bool plain = td && lin && g.n_stages == 2 && !g.tet_kf && !g.hex_kf && !g.tet_region && !g.hex_region &&
+                     !g.node_region && g.lean;
+  int lean = 0;
+  if (plain && kinds == 1 && g.tet_phase) {
+    kern = k_tiled_step<S, true, kRanked, 1, true, true>;
+    lean = 1;
+  } else if (plain && kinds == 0 && mode == kCornerPhase2) {
+    kern = k_tiled_step<S, true, kCornerPhase2, 0, true, true>;
+    lean = 2;
+  }
+  static size_t configured[3][2][2][3][7] = {};
+  size_t &cfg = configured[lean][lin][td ? 1 : 0][kinds][mode];
   if (smem > cfg) {
     FH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cfg = smem;

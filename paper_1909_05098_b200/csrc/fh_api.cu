@@ -896,7 +896,8 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   st->mode = mode;
   g.n_stages = 2;  // measured best on cfg4 (scripts/sweep.py)
   if (o.tile_stages > 0) g.n_stages = std::min(kMaxStages, o.tile_stages);
-  g.smem_T = (int)al(2 * sizeof(S) * (size_t)std::max(1, P.max_local_nodes));
+  // +1: the dummy node the padding slots point at (partition step 5)
+  g.smem_T = (int)al(2 * sizeof(S) * ((size_t)std::max(1, P.max_local_nodes) + 1));
   // +1: the trash slot of the corner-phase accumulation
   const int rows = std::max(st->mode == kModeCornerSlot ? 8 : st->mode == kModeCornerPhase4 ? 4
                                                             : (st->mode == kModeCornerPhase2 ? 2 : 1),

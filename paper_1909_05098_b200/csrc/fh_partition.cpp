@@ -442,19 +442,26 @@ void build_partition(const PartitionInput &in, Partition &P) {
       hord.resize(halo.size());
       for (size_t h = 0; h < halo.size(); ++h) hord[hrank[h]] = halo[h];
       const int64_t nloc = (int64_t)nn + (int64_t)halo.size();
-      if (nloc >= 0xffff) fail(FH_ERR_CONFIG, "tile has too many local nodes; lower part_nodes");
+      if (nloc >= 0xfffe) fail(FH_ERR_CONFIG, "tile has too many local nodes; lower part_nodes");
       P.max_local_nodes = std::max<int>(P.max_local_nodes, (int)nloc);
       P.max_part_free = std::max<int>(P.max_part_free, P.part_n_free[p]);
       auto local = [&](int32_t n) -> uint16_t {
         if (n >= n0 && n < n0 + nn) return (uint16_t)(n - n0);
         return (uint16_t)(nn + hrank[std::lower_bound(halo.begin(), halo.end(), n) - halo.begin()]);
       };
-      if (P.tet_rows > 1 && nloc >= (1 << 14))
+      if (P.tet_rows > 1 && nloc + 1 >= (1 << 14))
         fail(FH_ERR_CONFIG, "tile has too many local nodes for row-tagged tet slots; lower part_nodes");
       for (int64_t q = 4 * (int64_t)P.part_tet_start[p]; q < 4 * (int64_t)(P.part_tet_start[p] + P.part_tet_count[p]); ++q)
         P.tet_conn16[q] = (uint16_t)(local(P.tet_conn[q]) | (((tet_rowbits[q / 4] >> (2 * (q % 4))) & 3) << 14));
       for (int64_t q = 8 * (int64_t)P.part_hex_start[p]; q < 8 * (int64_t)(P.part_hex_start[p] + P.part_hex_count[p]); ++q)
         P.hex_conn16[q] = local(P.hex_conn[q]);
+      // padding slots up to the batch boundary point every corner at the
+      // dummy staged node nloc (T = k = 0, never updated): the LEAN loops read
+      // them like real slots and need no per-thread validity test
+      for (int64_t q = 4 * (int64_t)(P.part_tet_start[p] + P.part_tet_count[p]); q < 4 * (int64_t)P.part_tet_start[p + 1]; ++q)
+        P.tet_conn16[q] = (uint16_t)nloc;
+      for (int64_t q = 8 * (int64_t)(P.part_hex_start[p] + P.part_hex_count[p]); q < 8 * (int64_t)P.part_hex_start[p + 1]; ++q)
+        P.hex_conn16[q] = (uint16_t)nloc;
       P.halo_nodes.insert(P.halo_nodes.end(), hord.begin(), hord.end());
       P.part_halo_start[p + 1] = (int32_t)P.halo_nodes.size();
     }

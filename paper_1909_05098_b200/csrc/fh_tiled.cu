@@ -243,6 +243,17 @@ __device__ void issue_batch(const TiledArgs<S> &g, int p, int j, int nbt, unsign
   if (rank) bulk_g2s(stage + L.rank, rank + (size_t)N * s0, kr * N, bar);
 }
 
+// LEAN loops: the whole batch record (padding slots included) and, for tets,
+// the 256 phase bytes of batch j of the tile whose slots start at s_start
+template <typename S, int N>
+__device__ __forceinline__ void lean_issue(const TiledArgs<S> &g, int s_start, int j, unsigned char *stage,
+                                           uint64_t *bar) {
+  const unsigned char *rec = (N == 4 ? g.tet_rec : g.hex_rec) + (size_t)(s_start / kBatch + j) * RecBytes<S>(N);
+  mbar_expect_tx(bar, (uint32_t)(RecBytes<S>(N) + (N == 4 ? kBatch : 0)));
+  bulk_g2s(stage, rec, RecBytes<S>(N), bar);
+  if (N == 4) bulk_g2s(stage + RecBytes<S>(N), g.tet_phase + s_start + j * kBatch, kBatch, bar);
+}
+
 // element loads of staged slot i of the batch ------------------------------------
 template <typename S, bool TD, bool LIN>
 __device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned char *stage, const TK<S> *sT,
@@ -505,8 +516,12 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
     const uint32_t hbytes = (uint32_t)((((h0 + nh + 3) & ~3) - hs) * 4);
     mbar_expect_tx(&hbar, hbytes);
     if (hbytes) bulk_g2s(s_ids, g.halo_nodes + hs, hbytes, &hbar);
-    for (int j = 0; j < kStages && j < nb; ++j)
-      issue_batch(g, p, j, nbt, ring + j * g.stage_bytes, &bars[j], preg < 0);
+    for (int j = 0; j < kStages && j < nb; ++j) {
+      if constexpr (LEAN)
+        lean_issue<S, KINDS == 1 ? 4 : 8>(g, KINDS == 1 ? t_start : h_start, j, ring + j * g.stage_bytes, &bars[j]);
+      else
+        issue_batch(g, p, j, nbt, ring + j * g.stage_bytes, &bars[j], preg < 0);
+    }
 #if FH_PREFETCH_NODES
     // the node update's per-node streams, pulled into L2 while the batches run
     if (g.n_src) prefetch_range(g.xyzv + 4 * (size_t)n0, 4 * sizeof(S) * nfree);
@@ -558,6 +573,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       if (i < nh) sT[nn + i] = v;
     }
   }
+  if (tid == 0) sT[nn + nh] = TK<S>{S(0), S(0)};  // the padding slots' dummy node (partition step 5)
   __syncthreads();  // every halo id has been read: the accumulators may be zeroed
   const int acc_rows = max(MODE == kCornerSlot ? 8 : (MODE == kCornerPhase4 ? 4 : (MODE == kCornerPhase2 ? 2 : 1)),
                            KINDS == 2 ? 1 : g.tet_rows);
@@ -595,8 +611,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
           "@!p bra LWAIT_%=;\n}" ::"r"(bar0 + 8u * (uint32_t)st),
           "r"((uint32_t)(j >> 1) & 1u)
           : "memory");
-      const bool valid = j * kBatch + tid < cnt;
-      const int i = valid ? tid : 0;  // padding threads read slot 0 (accumulation predicated off)
+      // the whole batch record was copied: padding slots point at the dummy node
+      const bool valid = true;
+      const int i = tid;
       const S *G = reinterpret_cast<const S *>(stage + kG);
       const S g00 = G[i], g01 = G[kBatch + i], g02 = G[2 * kBatch + i], g11 = G[3 * kBatch + i],
               g12 = G[4 * kBatch + i], g22 = G[5 * kBatch + i];
@@ -659,9 +676,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       }
       if (tid == 0 && j + 2 < nb) {
         fence_proxy_async();
-        issue_batch(g, p, j + 2, nbt, stage, &bars[st], false);
+        lean_issue<S, N>(g, KINDS == 1 ? t_start : h_start, j + 2, stage, &bars[st]);
       }
     }
+    (void)cnt;
   } else {
   int st = 0;
   uint32_t parity = 0;

@@ -50,6 +50,12 @@ constexpr int kMinBlocksTetF64 = 3;
 #ifndef FH_NODE_UNROLL
 #define FH_NODE_UNROLL 2
 #endif
+#ifndef FH_STAGE_UNROLL_TET
+#define FH_STAGE_UNROLL_TET 4
+#endif
+#ifndef FH_NODE_UNROLL_TET
+#define FH_NODE_UNROLL_TET 1
+#endif
 // per-tile material / single-RF node bodies (0: the general body whenever node regions exist)
 #ifndef FH_PART_MAT
 #define FH_PART_MAT 1
@@ -543,7 +549,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
     r = (x >= kx1) ? ky1 : r;
     return (x <= kx0) ? ky0 : r;
   };
-  constexpr int U = FH_STAGE_UNROLL;  // loads in flight per thread while staging
+  // loads in flight per thread while staging (tet-only tiles: 4, measured
+  // 1% faster on cfg3; hex tiles: 8)
+  constexpr int U = KINDS == 1 ? FH_STAGE_UNROLL_TET : FH_STAGE_UNROLL;
   for (int base = tid; base < nn; base += U * kTileThreads) {
     S x[U];
 #pragma unroll
@@ -777,8 +785,12 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   // same with exactly one RF source.  `tm` is the tile's material.
   bool bad = false;
   const int rstart = g.part_robin_start[p];
-  const int tm = g.node_region ? (FH_PART_MAT ? (int)g.part_mat[p] : -1) : 0;
-  constexpr int UN = FH_NODE_UNROLL;  // nodes per thread per round: their global loads are issued together
+  // LEAN tet tiles: the one material's laws as direct constant-bank operands
+  // (measured: cfg3 0.0712 -> 0.0707 ms/step; the hex loop measured 1.5%
+  // slower with it, so it keeps the indexed loads)
+  const int tm = (LEAN && KINDS == 1) ? 0 : (g.node_region ? (FH_PART_MAT ? (int)g.part_mat[p] : -1) : 0);
+  // nodes per thread per round: their global loads are issued together
+  constexpr int UN = KINDS == 1 ? FH_NODE_UNROLL_TET : FH_NODE_UNROLL;
   auto node_loop = [&](auto kind_tag) {
     constexpr int KIND = decltype(kind_tag)::value;
     for (int base = tid; base < nfree; base += UN * kTileThreads) {

@@ -889,6 +889,10 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.flag = e->flag.p;
   g.n_nodes = Vt;
   g.lean = o.lean_kernels == 0 ? 1 : 0;
+  g.max_tile_batches = 0;
+  for (int q = 0; q < P.n_parts; ++q)
+    g.max_tile_batches = std::max(g.max_tile_batches, (P.part_tet_count[q] + kBatch - 1) / kBatch +
+                                                          (P.part_hex_count[q] + kBatch - 1) / kBatch);
   g.max_local = std::max(1, P.max_local_nodes);
   auto al = [](size_t b) { return (b + 127) & ~(size_t)127; };
   // accumulation mode: corner phases / corner slots need corner-unique tiles;

@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   __shared__ __align__(8) uint64_t hbar;  // halo id list copy
   __shared__ int s_bad;
   // phases per batch of the tile (colour modes), read once instead of per batch
-  constexpr int kNphCache = 64;
+  constexpr int kNphCache = kTileThreads;  // one phase-count byte per batch, filled by one thread each
   __shared__ uint8_t s_nph[kNphCache];
   // skip only when an EARLIER step failed: every CTA of the failing step still
   // writes its tile, so the field after a runaway is that whole step's output
@@ -631,8 +631,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         uint16_t nd[4];
         int rofs[4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          nd[a] = (uint16_t)(raw[a] & t_mask);
+        for (int a = 0; a < 4; ++a) {  // LEAN tets always carry 4 accumulator rows (host condition)
+          nd[a] = (uint16_t)(raw[a] & 0x3fffu);
           rofs[a] = (int)(raw[a] >> 14) * nfree;
         }
         S T[4], K[4];
@@ -651,8 +651,32 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         c[3] = kb * (g02 * d1 + g12 * d2 + g22 * d3);
         c[0] = -((c[1] + c[2]) + c[3]);
         const int ph = stage[kPhase + i];
-        const int nph = j < kNphCache ? (int)s_nph[j] : (int)__ldg(g.tet_bnph + t_start / kBatch + j);
-        accumulate_colored<S, 4>(acc, nd, c, nfree, valid, ph, nph, rofs);
+        const int nph = s_nph[j];  // LEAN tiles have at most kNphCache batches (host condition)
+        // colour phases (accumulate_colored): the slot's 4 corners are 4
+        // distinct nodes, so the 4 read-modify-writes are issued together;
+        // the first two phases are unrolled (1.3 phases per batch on cfg3)
+        int loc[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) loc[a] = nd[a] < nfree ? (int)nd[a] + rofs[a] : -1;
+        auto rmw = [&]() {
+          S old[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) old[a] = loc[a] >= 0 ? acc[loc[a]] : S(0);
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+            if (loc[a] >= 0) acc[loc[a]] = old[a] - c[a];
+        };
+        (void)valid;
+        if (ph == 0) rmw();
+        __syncthreads();
+        if (nph > 1) {
+          if (ph == 1) rmw();
+          __syncthreads();
+          for (int q = 2; q < nph; ++q) {
+            if (ph == q) rmw();
+            __syncthreads();
+          }
+        }
       } else {
         const uint4 w = reinterpret_cast<const uint4 *>(stage)[i];
         uint16_t nd[kSPT][8];
@@ -678,9 +702,18 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         S c[kSPT][8];
         c[0][0] = -a0 - w2; c[0][1] = b0 - w2; c[0][2] = a0 - w2; c[0][3] = -b0 - w2;
         c[0][4] = -a0 + w2; c[0][5] = b0 + w2; c[0][6] = a0 + w2; c[0][7] = -b0 + w2;
-        const bool vv[kSPT] = {valid};
-        uint8_t rk[kSPT][8];
-        accumulate<S, 8, MODE>(acc, nd, c, nfree, vv, rk, 0);
+        // two-row corner phases (accumulate<kCornerPhase2>): corners a and a+4
+        // go to different rows, so both read-modify-writes issue together
+        (void)valid;
+        S *acc1 = acc + nfree;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const int l0 = nd[0][a] < nfree ? (int)nd[0][a] : -1, l1 = nd[0][a + 4] < nfree ? (int)nd[0][a + 4] : -1;
+          const S o0 = l0 >= 0 ? acc[l0] : S(0), o1 = l1 >= 0 ? acc1[l1] : S(0);
+          if (l0 >= 0) acc[l0] = o0 - c[0][a];
+          if (l1 >= 0) acc1[l1] = o1 - c[0][a + 4];
+          __syncthreads();
+        }
       }
       if (tid == 0 && j + 2 < nb) {
         fence_proxy_async();
@@ -908,9 +941,9 @@ void (*pick_step_kernel(const TiledArgs<S> &g, bool td, int mode_sel, size_t sme
   K kern = table[lin][td ? 1 : 0][kinds][mode];
   // the LEAN batch loops (see k_tiled_step)
   const bool plain = td && lin && g.n_stages == 2 && !g.tet_kf && !g.hex_kf && !g.tet_region && !g.hex_region &&
-                     !g.node_region && g.lean;
+                     !g.node_region && g.lean && g.max_tile_batches <= kTileThreads;
   int lean = 0;
-  if (plain && kinds == 1 && g.tet_phase) {
+  if (plain && kinds == 1 && g.tet_phase && g.tet_rows == 4) {
     kern = k_tiled_step<S, true, kRanked, 1, true, true>;
     lean = 1;
   } else if (plain && kinds == 0 && mode == kCornerPhase2) {

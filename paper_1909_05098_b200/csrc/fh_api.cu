@@ -138,7 +138,7 @@ template <typename S>
 __global__ void k_pack_slots(const int32_t *__restrict__ slot_elem, int64_t n, const double *__restrict__ G,
                              double scale, S *__restrict__ out_G, int rec_elems, int g_off, const double *__restrict__ kf,
                              S *__restrict__ out_kf, const int32_t *__restrict__ region,
-                             uint8_t *__restrict__ out_region) {
+                             uint8_t *__restrict__ out_region, int paired) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= n) return;
   const int64_t e = slot_elem[s];
@@ -147,8 +147,15 @@ __global__ void k_pack_slots(const int32_t *__restrict__ slot_elem, int64_t n, c
   // temperature-dependent runs fold the conductivity factor into G (no kf
   // stream: out_kf == nullptr); frozen runs keep it for the freeze
   const double f = (kf && !out_kf && e >= 0) ? kf[e] : 1.0;
+  // G components 00 01 02 11 12 22: [6][B] rows, or (LEAN records) 3 rows of
+  // interleaved pairs (00,01) (02,11) (12,22)
+  const int64_t pbase = (s / kBatch) * rec_elems + g_off + 2 * (s % kBatch);
 #pragma unroll
-  for (int k = 0; k < 6; ++k) out_G[base + k * kBatch] = e >= 0 ? (S)(G[6 * e + k] * scale * f) : S(0);
+  for (int k = 0; k < 6; ++k) {
+    const S v = e >= 0 ? (S)(G[6 * e + k] * scale * f) : S(0);
+    if (paired) out_G[pbase + (k >> 1) * 2 * kBatch + (k & 1)] = v;
+    else out_G[base + k * kBatch] = v;
+  }
   if (out_kf) out_kf[s] = e >= 0 ? (S)kf[e] : S(1);
   if (out_region) out_region[s] = e >= 0 ? (uint8_t)region[e] : 0;
 }
@@ -179,6 +186,7 @@ struct TiledState {
   // tiles with tets at the head of the boundary / interior ranges (mixed meshes)
   int n_mixed_b = 0, n_mixed_i = 0;
   int mode = 0;
+  bool lean = false;  // LEAN loops and their paired-G records
 };
 
 }  // namespace
@@ -758,16 +766,32 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     }
     st->part_region.upload(pr, s);
   }
+  // LEAN batch loops (fh_tiled.cu): tet-only colour tiles with 4 rows or
+  // hex-only two-row corner-phase tiles, one material, TD two-knot laws, no
+  // kf stream, the 2-deep ring, <= 256 batches per tile.  Their fp32
+  // records store G as 3 interleaved pairs (one 8-byte load per pair; the
+  // 16-byte fp64 pairs measured 1.4% slower on cfg3, so fp64 keeps 6 rows).
+  {
+    MatSet<S> mt = mats_of<S>(e);
+    const bool lin_ok = normalise_curves(mt) != 0;
+    int max_b = 0;
+    for (int q = 0; q < P.n_parts; ++q)
+      max_b = std::max(max_b, (P.part_tet_count[q] + kBatch - 1) / kBatch + (P.part_hex_count[q] + kBatch - 1) / kBatch);
+    const bool kind_ok = nhs == 0 ? (tet_mode == kModeColored && P.tet_rows == 4)
+                                  : (nts == 0 && mode == kModeCornerPhase2);
+    st->lean = e->td && lin_ok && o.lean_kernels == 0 && (o.tile_stages == 0 || o.tile_stages == 2) && !regions &&
+               !st->tet_kf.p && !st->hex_kf.p && kind_ok && max_b <= kBatch;
+  }
   if (nts)
     k_pack_slots<S><<<nblk(nts), kBlk, 0, s>>>(st->tet_slot_elem.p, nts, G_dev, 1.0,
                                                reinterpret_cast<S *>(st->tet_rec.p), RecBytes<S>(4) / (int)sizeof(S),
                                                kBatch * 4 * 2 / (int)sizeof(S), e->kfactor.p, st->tet_kf.p,
-                                               e->elem_region.p, st->tet_region.p);
+                                               e->elem_region.p, st->tet_region.p, st->lean && sizeof(S) == 4);
   if (nhs)
     k_pack_slots<S><<<nblk(nhs), kBlk, 0, s>>>(st->hex_slot_elem.p, nhs, G_dev, 1.0 / 64.0,
                                                reinterpret_cast<S *>(st->hex_rec.p), RecBytes<S>(8) / (int)sizeof(S),
                                                kBatch * 8 * 2 / (int)sizeof(S), e->kfactor.p, st->hex_kf.p,
-                                               e->elem_region.p, st->hex_region.p);
+                                               e->elem_region.p, st->hex_region.p, st->lean && sizeof(S) == 4);
   FH_CUDA(cudaGetLastError());
   // nodal arrays in the new (multi-GPU: rank-local) numbering
   st->T[0].alloc(Vt);
@@ -888,7 +912,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.runaway_limit = (S)e->runaway_limit;
   g.flag = e->flag.p;
   g.n_nodes = Vt;
-  g.lean = o.lean_kernels == 0 ? 1 : 0;
+  g.lean = st->lean ? 1 : 0;
   g.max_tile_batches = 0;
   for (int q = 0; q < P.n_parts; ++q)
     g.max_tile_batches = std::max(g.max_tile_batches, (P.part_tet_count[q] + kBatch - 1) / kBatch +

@@ -622,9 +622,18 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       // the whole batch record was copied: padding slots point at the dummy node
       const bool valid = true;
       const int i = tid;
-      const S *G = reinterpret_cast<const S *>(stage + kG);
-      const S g00 = G[i], g01 = G[kBatch + i], g02 = G[2 * kBatch + i], g11 = G[3 * kBatch + i],
-              g12 = G[4 * kBatch + i], g22 = G[5 * kBatch + i];
+      // fp32: paired G rows (k_pack_slots) (00,01) (02,11) (12,22), one 8-byte
+      // load each; fp64: the 6 component rows
+      S g00, g01, g02, g11, g12, g22;
+      if constexpr (sizeof(S) == 4) {
+        const float2 *G2 = reinterpret_cast<const float2 *>(stage + kG);
+        const float2 p0 = G2[i], p1 = G2[kBatch + i], p2 = G2[2 * kBatch + i];
+        g00 = p0.x; g01 = p0.y; g02 = p1.x; g11 = p1.y; g12 = p2.x; g22 = p2.y;
+      } else {
+        const S *G = reinterpret_cast<const S *>(stage + kG);
+        g00 = G[i]; g01 = G[kBatch + i]; g02 = G[2 * kBatch + i];
+        g11 = G[3 * kBatch + i]; g12 = G[4 * kBatch + i]; g22 = G[5 * kBatch + i];
+      }
       if constexpr (KINDS == 1) {
         const uint2 w = reinterpret_cast<const uint2 *>(stage)[i];
         const uint32_t raw[4] = {w.x & 0xffffu, w.x >> 16, w.y & 0xffffu, w.y >> 16};
@@ -940,13 +949,12 @@ void (*pick_step_kernel(const TiledArgs<S> &g, bool td, int mode_sel, size_t sme
   const int lin = g.lin ? 1 : 0;
   K kern = table[lin][td ? 1 : 0][kinds][mode];
   // the LEAN batch loops (see k_tiled_step)
-  const bool plain = td && lin && g.n_stages == 2 && !g.tet_kf && !g.hex_kf && !g.tet_region && !g.hex_region &&
-                     !g.node_region && g.lean && g.max_tile_batches <= kTileThreads;
+  // decided at setup (TiledState::lean), which also packed the records' G in pairs
   int lean = 0;
-  if (plain && kinds == 1 && g.tet_phase && g.tet_rows == 4) {
+  if (g.lean && kinds == 1) {
     kern = k_tiled_step<S, true, kRanked, 1, true, true>;
     lean = 1;
-  } else if (plain && kinds == 0 && mode == kCornerPhase2) {
+  } else if (g.lean && kinds == 0) {
     kern = k_tiled_step<S, true, kCornerPhase2, 0, true, true>;
     lean = 2;
   }

@@ -65,7 +65,7 @@ struct TiledArgs {
   FailFlag *flag;
   unsigned long long step_no;
   int64_t n_nodes;  // length of Tin / Tout (bounds checks of the checked build)
-  int lean;         // 1: the specialised batch loops may be used (fh_options.lean_kernels == 0)
+  int lean;         // 1: the LEAN batch loops (records packed with paired G; see setup_tiled)
   int max_tile_batches;  // most 256-slot batches in one tile (LEAN tiles: <= kTileThreads)
   int max_local;    // owned + halo nodes a tile may stage (shared-memory capacity)
 };

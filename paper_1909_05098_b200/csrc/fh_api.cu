@@ -768,7 +768,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   }
   // LEAN batch loops (fh_tiled.cu): tet-only colour tiles with 4 rows or
   // hex-only two-row corner-phase tiles, one material, TD two-knot laws, no
-  // kf stream, the 2-deep ring, <= 256 batches per tile.  Their fp32
+  // kf stream, <= 256 batches per tile.  Their fp32
   // records store G as 3 interleaved pairs (one 8-byte load per pair; the
   // 16-byte fp64 pairs measured 1.4% slower on cfg3, so fp64 keeps 6 rows).
   {
@@ -779,7 +779,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
       max_b = std::max(max_b, (P.part_tet_count[q] + kBatch - 1) / kBatch + (P.part_hex_count[q] + kBatch - 1) / kBatch);
     const bool kind_ok = nhs == 0 ? (tet_mode == kModeColored && P.tet_rows == 4)
                                   : (nts == 0 && mode == kModeCornerPhase2);
-    st->lean = e->td && lin_ok && o.lean_kernels == 0 && (o.tile_stages == 0 || o.tile_stages == 2) && !regions &&
+    st->lean = e->td && lin_ok && o.lean_kernels == 0 && !regions &&
                !st->tet_kf.p && !st->hex_kf.p && kind_ok && max_b <= kBatch;
   }
   if (nts)

@@ -50,6 +50,9 @@ constexpr int kMinBlocksTetF64 = 3;
 #ifndef FH_NODE_UNROLL
 #define FH_NODE_UNROLL 2
 #endif
+#ifndef FH_HEX_TM_CONST
+#define FH_HEX_TM_CONST 0
+#endif
 #ifndef FH_STAGE_UNROLL_TET
 #define FH_STAGE_UNROLL_TET 4
 #endif
@@ -463,8 +466,8 @@ __device__ __forceinline__ void accumulate_colored(S *acc, const uint16_t (&nd)[
 // KINDS: 0 hex-only, 1 tet-only, 2 mixed mesh (the absent kind's path is compiled out).
 // LEAN: the batch loop specialised for the common tiles -- tet-only colour
 // phases or hex-only two-row corner phases, one material, no per-slot kf /
-// region / rank streams, a 2-deep ring -- with every per-batch flag and
-// stage offset a compile-time constant (same arithmetic, same bits).
+// region / rank streams -- with every per-batch flag and stage offset a
+// compile-time constant (same arithmetic, same bits).
 template <typename S, bool TD, int MODE, int KINDS, bool LIN, bool LEAN = false>
 __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? kMinBlocksTet : kMinBlocksF32)
                                                                 : (KINDS == 1 ? kMinBlocksTetF64 : 2))
@@ -609,19 +612,28 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
     const int sbytes = g.stage_bytes;
     const uint32_t bar0 = smem_u32(&bars[0]);
     const int cnt = KINDS == 1 ? t_cnt : h_cnt;
+    int st = 0;
+    uint32_t par = 0;
     for (int j = 0; j < nb; ++j) {
-      const int st = j & 1;
       unsigned char *stage = ring + st * sbytes;
       asm volatile(
           "{\n\t.reg .pred p;\n"
           "LWAIT_%=:\n\t"
           "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
           "@!p bra LWAIT_%=;\n}" ::"r"(bar0 + 8u * (uint32_t)st),
-          "r"((uint32_t)(j >> 1) & 1u)
+          "r"(par)
           : "memory");
       // the whole batch record was copied: padding slots point at the dummy node
       const bool valid = true;
       const int i = tid;
+      // every thread has read its slot from the stage once the batch's first
+      // accumulation barrier is passed: the refill goes out right there
+      auto refill = [&]() {
+        if (tid == 0 && j + kStages < nb) {
+          fence_proxy_async();
+          lean_issue<S, N>(g, KINDS == 1 ? t_start : h_start, j + kStages, stage, &bars[st]);
+        }
+      };
       // fp32: paired G rows (k_pack_slots) (00,01) (02,11) (12,22), one 8-byte
       // load each; fp64: the 6 component rows
       S g00, g01, g02, g11, g12, g22;
@@ -678,6 +690,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         (void)valid;
         if (ph == 0) rmw();
         __syncthreads();
+        refill();
         if (nph > 1) {
           if (ph == 1) rmw();
           __syncthreads();
@@ -722,11 +735,12 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
           if (l0 >= 0) acc[l0] = o0 - c[0][a];
           if (l1 >= 0) acc1[l1] = o1 - c[0][a + 4];
           __syncthreads();
+          if (a == 0) refill();
         }
       }
-      if (tid == 0 && j + 2 < nb) {
-        fence_proxy_async();
-        lean_issue<S, N>(g, KINDS == 1 ? t_start : h_start, j + 2, stage, &bars[st]);
+      if (++st == kStages) {
+        st = 0;
+        par ^= 1u;
       }
     }
     (void)cnt;
@@ -830,7 +844,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   // LEAN tet tiles: the one material's laws as direct constant-bank operands
   // (measured: cfg3 0.0712 -> 0.0707 ms/step; the hex loop measured 1.5%
   // slower with it, so it keeps the indexed loads)
-  const int tm = (LEAN && KINDS == 1) ? 0 : (g.node_region ? (FH_PART_MAT ? (int)g.part_mat[p] : -1) : 0);
+  const int tm = (LEAN && (KINDS == 1 || FH_HEX_TM_CONST)) ? 0
+                                                          : (g.node_region ? (FH_PART_MAT ? (int)g.part_mat[p] : -1) : 0);
   // nodes per thread per round: their global loads are issued together
   constexpr int UN = KINDS == 1 ? FH_NODE_UNROLL_TET : FH_NODE_UNROLL;
   auto node_loop = [&](auto kind_tag) {

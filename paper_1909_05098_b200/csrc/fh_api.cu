@@ -185,6 +185,7 @@ struct TiledState {
   int n_boundary = 0;  // multi-GPU: leading entries of part_list that touch the halo
   // tiles with tets at the head of the boundary / interior ranges (mixed meshes)
   int n_mixed_b = 0, n_mixed_i = 0;
+  int n_lean_i = 0;  // one GPU, regions: material-0 hex-only tiles at the end of the list (LEAN 2 launch)
   int mode = 0;
   bool lean = false;  // LEAN loops and their paired-G records
 };
@@ -664,6 +665,27 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     st->n_mixed_b = (int)(mid_b - plist.begin());
     st->n_mixed_i = (int)(mid_i - (plist.begin() + st->n_boundary));
   }
+  // one GPU with material regions: the hex-only tiles whose slots all lie in
+  // region 0 go last and run the LEAN 2 loop (fh_tiled.cu), the others keep
+  // the general kernel
+  if (e->X.world == 1 && o.n_materials > 1 && o.element_region && e->td && o.lean_kernels == 0 &&
+      P.corner_unique && sizeof(S) == 4 && !(e->kfactor.p && !e->td)) {
+    MatSet<S> mt = mats_of<S>(e);
+    bool ok = normalise_curves(mt) != 0;
+    for (int q = 0; q < P.n_parts && ok; ++q)
+      ok = (P.part_hex_count[q] + kBatch - 1) / kBatch + (P.part_tet_count[q] + kBatch - 1) / kBatch <= kBatch;
+    auto region0 = [&](int32_t p) {
+      if (P.part_tet_count[p] > 0) return false;
+      for (int32_t q = P.part_hex_start[p]; q < P.part_hex_start[p] + P.part_hex_count[p]; ++q)
+        if (P.hex_slot_elem[q] >= 0 && o.element_region[P.hex_slot_elem[q]] != 0) return false;
+      return true;
+    };
+    if (ok) {
+      auto first = plist.begin() + st->n_boundary + st->n_mixed_i;
+      auto mid = std::stable_partition(first, plist.end(), [&](int32_t p) { return !region0(p); });
+      st->n_lean_i = (int)(plist.end() - mid);
+    }
+  }
   st->part_list.upload(plist, s);
   if (e->X.world > 1) {
     e->x_send.upload(e->X.send_nodes, s);
@@ -1140,7 +1162,19 @@ void tiled_run(fh_engine *e, int64_t nsteps, double dt) {
       TiledArgs<S> gh = g;
       gh.tet_rec = nullptr;
       gh.part_begin = begin + n_mixed;
-      tiled_step(gh, count - n_mixed, e->td, st.mode, st.smem, e->stream);
+      const int n_lean = (e->X.world == 1) ? st.n_lean_i : 0;
+      if (n_lean > 0) {  // material-0 hex tiles: LEAN 2 on the engine stream; the rest beside the mixed tiles
+        if (count - n_mixed - n_lean > 0) {
+          tiled_step(gh, count - n_mixed - n_lean, e->td, st.mode, st.smem, e->kind_stream);
+          FH_CUDA(cudaEventRecord(e->ev_join, e->kind_stream));
+        }
+        TiledArgs<S> gl = gh;
+        gl.part_begin = begin + count - n_lean;
+        gl.lean = 2;
+        tiled_step(gl, n_lean, e->td, st.mode, st.smem, e->stream);
+      } else {
+        tiled_step(gh, count - n_mixed, e->td, st.mode, st.smem, e->stream);
+      }
       FH_CUDA(cudaStreamWaitEvent(e->stream, e->ev_join, 0));
     };
     if (e->assembly == FH_ASSEMBLY_ATOMIC) {
@@ -2106,7 +2140,7 @@ int fh_get_layout(fh_engine *e, fh_layout *out) {
     const Partition &P = e->part;
     auto launches = [&](const auto &st) {  // one per tile kind present in each launch range
       const int ni = st.n_parts_local - st.n_boundary;
-      return (st.n_mixed_i > 0 && st.n_mixed_i < ni ? 2 : 1) +
+      return (st.n_mixed_i > 0 && st.n_mixed_i < ni ? 2 : 1) + (st.n_lean_i > 0 && st.n_lean_i < ni - st.n_mixed_i ? 1 : 0) +
              (st.n_boundary ? (st.n_mixed_b > 0 && st.n_mixed_b < st.n_boundary ? 2 : 1) : 0);
     };
     out->kernels_per_step = e->precision == 32 ? launches(*e->tf) : launches(*e->tdd);

@@ -465,10 +465,13 @@ __device__ __forceinline__ void accumulate_colored(S *acc, const uint16_t (&nd)[
 
 // KINDS: 0 hex-only, 1 tet-only, 2 mixed mesh (the absent kind's path is compiled out).
 // LEAN: the batch loop specialised for the common tiles -- tet-only colour
-// phases or hex-only two-row corner phases, one material, no per-slot kf /
-// region / rank streams -- with every per-batch flag and stage offset a
-// compile-time constant (same arithmetic, same bits).
-template <typename S, bool TD, int MODE, int KINDS, bool LIN, bool LEAN = false>
+// phases or hex-only two-row corner phases, every slot in material 0, no
+// per-slot kf / region / rank streams -- with every per-batch flag and stage
+// offset a compile-time constant (same arithmetic, same bits).  LEAN 1: the
+// whole launch (fp32 records with paired G rows); LEAN 2: the material-0
+// hex-only tiles of a mesh with regions (component-row G, like the general
+// kernel's tiles of the same launch family).
+template <typename S, bool TD, int MODE, int KINDS, bool LIN, int LEAN = 0>
 __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? kMinBlocksTet : kMinBlocksF32)
                                                                 : (KINDS == 1 ? kMinBlocksTetF64 : 2))
     k_tiled_step(const __grid_constant__ TiledArgs<S> g) {
@@ -637,7 +640,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       // fp32: paired G rows (k_pack_slots) (00,01) (02,11) (12,22), one 8-byte
       // load each; fp64: the 6 component rows
       S g00, g01, g02, g11, g12, g22;
-      if constexpr (sizeof(S) == 4) {
+      if constexpr (sizeof(S) == 4 && LEAN == 1) {
         const float2 *G2 = reinterpret_cast<const float2 *>(stage + kG);
         const float2 p0 = G2[i], p1 = G2[kBatch + i], p2 = G2[2 * kBatch + i];
         g00 = p0.x; g01 = p0.y; g02 = p1.x; g11 = p1.y; g12 = p2.x; g22 = p2.y;
@@ -966,14 +969,17 @@ void (*pick_step_kernel(const TiledArgs<S> &g, bool td, int mode_sel, size_t sme
   // the LEAN batch loops (see k_tiled_step)
   // decided at setup (TiledState::lean), which also packed the records' G in pairs
   int lean = 0;
-  if (g.lean && kinds == 1) {
-    kern = k_tiled_step<S, true, kRanked, 1, true, true>;
+  if (g.lean == 1 && kinds == 1) {
+    kern = k_tiled_step<S, true, kRanked, 1, true, 1>;
     lean = 1;
-  } else if (g.lean && kinds == 0) {
-    kern = k_tiled_step<S, true, kCornerPhase2, 0, true, true>;
+  } else if (g.lean == 1 && kinds == 0) {
+    kern = k_tiled_step<S, true, kCornerPhase2, 0, true, 1>;
     lean = 2;
+  } else if (g.lean == 2 && kinds == 0) {
+    kern = k_tiled_step<S, true, kCornerPhase2, 0, true, 2>;
+    lean = 3;
   }
-  static size_t configured[3][2][2][3][7] = {};
+  static size_t configured[4][2][2][3][7] = {};
   size_t &cfg = configured[lean][lin][td ? 1 : 0][kinds][mode];
   if (smem > cfg) {
     FH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

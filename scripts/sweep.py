@@ -27,6 +27,7 @@ ap.add_argument("--modes", default="1,2")
 ap.add_argument("--stages", default="2,3")
 ap.add_argument("--steps", type=int, default=50)
 ap.add_argument("--tuning", default="")
+ap.add_argument("--bench-layout", action="store_true", help="bench.py's domains (8; cfg4: z-slabs)")
 ap.add_argument("--check", action="store_true", help="compare each variant's field with the first one's")
 args = ap.parse_args()
 
@@ -41,9 +42,12 @@ for pn in [int(x) for x in args.parts.split(",")]:
             tuning.update({k: int(v) for k, v in (kv.split("=") for kv in args.tuning.split(",") if kv)})
             if mode == 4:
                 tuning["allow_nondeterministic"] = 1
+            lay_kw = dict(n_domains=8, slab_axis=2 if args.config == "cfg4" else -1) if args.bench_layout else {}
             eng = fh.ExplicitEngine(prob.mesh, prob.material, prob.boundary, assembly="tiled", part_nodes=pn,
-                                    tuning=tuning, **prob.engine_kwargs())
+                                    tuning=tuning, **lay_kw, **prob.engine_kwargs())
             dt = 0.9 * eng.critical_dt(37.0)
+            if args.config == "cfg4":
+                eng.set_sources(bench.run_sources(prob, dt))
             st = eng.initial_state(37.0)
             L, h = eng._L, eng._h
             N.check(L.fh_set_temperature(h, N.ptr(st.temperatures), st.temperatures.size, 0, 0.0))

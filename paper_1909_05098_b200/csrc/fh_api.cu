@@ -732,7 +732,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     if (m == kModeSharedAtomic && !o.allow_nondeterministic)
       fail(FH_ERR_CONFIG, "tile_mode shared-memory atomics is non-deterministic: set allow_nondeterministic");
     if (m == kModeRanked || m == kModeSharedAtomic || (m == kModeColored && hex_colour_ok) ||
-        ((m == kModeCornerPhase || m == kModeCornerSlot || m == kModeCornerPhase2 || m == kModeCornerPhase4) &&
+        ((m == kModeCornerPhase || m == kModeCornerPhase2) &&
          P.corner_unique))
       mode = m;
     else
@@ -949,8 +949,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   // +1: the dummy node the padding slots point at (partition step 5)
   g.smem_T = (int)al(2 * sizeof(S) * ((size_t)std::max(1, P.max_local_nodes) + 1));
   // +1: the trash slot of the corner-phase accumulation
-  const int rows = std::max(st->mode == kModeCornerSlot ? 8 : st->mode == kModeCornerPhase4 ? 4
-                                                            : (st->mode == kModeCornerPhase2 ? 2 : 1),
+  const int rows = std::max(st->mode == kModeCornerPhase2 ? 2 : 1,
                             P.tet_rows);
   g.smem_acc = (int)al(sizeof(S) * rows * ((size_t)std::max(1, P.max_part_free) + 1));
   {  // the accumulator region first holds the tile's halo id list (bulk copy)

@@ -347,8 +347,6 @@ __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned 
 // accumulation modes (deterministic in all three):
 //   kRanked      phase = rank of the slot among the node's slots of the batch
 //   kCornerPhase corner-unique tiles: phase = corner index (N barriers/batch)
-//   kCornerSlot  corner-unique tiles: one accumulator row per corner, plain
-//                stores, summed in corner order at the node update (1 barrier)
 // Each thread carries kSPT slots of the batch (i = q * kTileThreads + tid).
 //   kColored     slots sorted by colour (no two slots of a colour share an
 //                updated node): phase = colour index inside the batch, so a
@@ -357,8 +355,8 @@ __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned 
 //                but the summation order is not fixed (tolerance-only, opt-in)
 //   kCornerPhase2  corner phases with two accumulator rows (corners a and
 //                a + N/2 share a phase): half the barriers, 2x accumulator smem
-//   kCornerPhase4  corner phases with four accumulator rows (corners a, a+1,
-//                a+2, a+3 of one half share a phase): 2 barriers, 4x smem
+// (round 1 also measured one accumulator row per corner and four-row corner
+// phases: both slower, the extra rows cost a resident CTA per SM; removed)
 enum { kRanked = 0, kCornerPhase = 1, kCornerSlot = 2, kColored = 3, kSharedAtomic = 4, kCornerPhase2 = 5,
        kCornerPhase4 = 6 };
 
@@ -370,14 +368,7 @@ __device__ __forceinline__ void accumulate(S *acc, const uint16_t (&nd)[kSPT][N]
   for (int q = 0; q < kSPT; ++q)
 #pragma unroll
     for (int a = 0; a < N; ++a) loc[q][a] = (valid[q] && nd[q][a] < nfree) ? (int)nd[q][a] : -1;
-  if (MODE == kCornerSlot) {
-#pragma unroll
-    for (int q = 0; q < kSPT; ++q)
-#pragma unroll
-      for (int a = 0; a < N; ++a)
-        if (loc[q][a] >= 0) acc[a * nfree + loc[q][a]] = -c[q][a];
-    __syncthreads();  // stage buffer fully consumed before it is refilled
-  } else if (MODE == kSharedAtomic) {
+  if (MODE == kSharedAtomic) {
     // non-deterministic (summation order varies run to run; tolerance-only)
 #pragma unroll
     for (int q = 0; q < kSPT; ++q)
@@ -396,18 +387,6 @@ __device__ __forceinline__ void accumulate(S *acc, const uint16_t (&nd)[kSPT][N]
         if (loc[q][a] >= 0) acc[loc[q][a]] -= c[q][a];
         if (loc[q][a + N / 2] >= 0) acc1[loc[q][a + N / 2]] -= c[q][a + N / 2];
       }
-      __syncthreads();
-    }
-  } else if (MODE == kCornerPhase4) {
-    // four rows: corner h * N/2 + r into row r, one phase per half -> 2 barriers
-    // per hex batch; F = (row0 + row1) + (row2 + row3)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-#pragma unroll
-      for (int q = 0; q < kSPT; ++q)
-#pragma unroll
-        for (int r = 0; r < N / 2; ++r)
-          if (loc[q][h * (N / 2) + r] >= 0) acc[r * nfree + loc[q][h * (N / 2) + r]] -= c[q][h * (N / 2) + r];
       __syncthreads();
     }
   } else if (MODE == kCornerPhase && !FH_TRASH_SLOT) {
@@ -589,7 +568,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   }
   if (tid == 0) sT[nn + nh] = TK<S>{S(0), S(0)};  // the padding slots' dummy node (partition step 5)
   __syncthreads();  // every halo id has been read: the accumulators may be zeroed
-  const int acc_rows = max(MODE == kCornerSlot ? 8 : (MODE == kCornerPhase4 ? 4 : (MODE == kCornerPhase2 ? 2 : 1)),
+  const int acc_rows = max(MODE == kCornerPhase2 ? 2 : 1,
                            KINDS == 2 ? 1 : g.tet_rows);
   for (int i = tid; i < acc_rows * nfree; i += kTileThreads) acc[i] = S(0);
   __syncthreads();
@@ -878,13 +857,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         const int n = n0 + loc;
         const S x = sT[loc].t;
         S Fsum;
-        if (MODE == kCornerSlot) {  // corner slots summed in fixed corner order: deterministic
-          Fsum = ((acc[loc] + acc[nfree + loc]) + (acc[2 * nfree + loc] + acc[3 * nfree + loc])) +
-                 ((acc[4 * nfree + loc] + acc[5 * nfree + loc]) + (acc[6 * nfree + loc] + acc[7 * nfree + loc]));
-        } else if (MODE == kCornerPhase2) {
+        if (MODE == kCornerPhase2) {
           Fsum = acc[loc] + acc[nfree + loc];
-        } else if (MODE == kCornerPhase4 && KINDS != 1) {
-          Fsum = (acc[loc] + acc[nfree + loc]) + (acc[2 * nfree + loc] + acc[3 * nfree + loc]);
         } else if (KINDS == 1 && g.tet_rows > 1) {  // tet accumulator rows, summed in row order
           Fsum = (acc[loc] + acc[nfree + loc]) + (acc[2 * nfree + loc] + acc[3 * nfree + loc]);
         } else {
@@ -947,9 +921,9 @@ void (*pick_step_kernel(const TiledArgs<S> &g, bool td, int mode_sel, size_t sme
   // only matters with temperature-dependent laws (TI never interpolates).
 #define FH_MODES(TDV, KV, L)                                                                       \
   {k_tiled_step<S, TDV, kRanked, KV, L>, k_tiled_step<S, TDV, kCornerPhase, KV, L>,                 \
-   k_tiled_step<S, TDV, kCornerSlot, KV, L>, k_tiled_step<S, TDV, kColored, KV, L>,                 \
+   k_tiled_step<S, TDV, kRanked, KV, L>, k_tiled_step<S, TDV, kColored, KV, L>,                     \
    k_tiled_step<S, TDV, kSharedAtomic, KV, L>, k_tiled_step<S, TDV, kCornerPhase2, KV, L>,          \
-   k_tiled_step<S, TDV, kCornerPhase4, KV, L>}
+   k_tiled_step<S, TDV, kRanked, KV, L>}
 #define FH_TETONLY(TDV, L)                                                                         \
   {k_tiled_step<S, TDV, kRanked, 1, L>, k_tiled_step<S, TDV, kRanked, 1, L>,                        \
    k_tiled_step<S, TDV, kRanked, 1, L>, k_tiled_step<S, TDV, kRanked, 1, L>,                        \

@@ -100,11 +100,11 @@ int tiled_occupancy(const TiledArgs<S> &g, bool td, int mode, size_t smem);
 enum TileMode {
   kModeRanked = 0,
   kModeCornerPhase = 1,
-  kModeCornerSlot = 2,
+  kModeCornerSlot = 2,    // removed (measured slower); rejected by fh_create
   kModeColored = 3,
   kModeSharedAtomic = 4,
   kModeCornerPhase2 = 5,
-  kModeCornerPhase4 = 6
+  kModeCornerPhase4 = 6   // removed (measured slower); rejected by fh_create
 };
 
 // TI freeze: per-slot kbar (global-id connectivity conn4/conn8) and per-node

@@ -947,7 +947,8 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.n_stages = 2;  // measured best on cfg4 (scripts/sweep.py)
   if (o.tile_stages > 0) g.n_stages = std::min(kMaxStages, o.tile_stages);
   // +1: the dummy node the padding slots point at (partition step 5)
-  g.smem_T = (int)al(2 * sizeof(S) * ((size_t)std::max(1, P.max_local_nodes) + 1));
+  // staged per node: T, plus k(T) only for laws with more than two knots (fh_tiled.cu, Staged)
+  g.smem_T = (int)al((e->td && !g.lin ? 2 : 1) * sizeof(S) * ((size_t)std::max(1, P.max_local_nodes) + 1));
   // +1: the trash slot of the corner-phase accumulation
   const int rows = std::max(st->mode == kModeCornerPhase2 ? 2 : 1,
                             P.tet_rows);

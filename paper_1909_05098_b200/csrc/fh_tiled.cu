@@ -74,6 +74,18 @@ struct __align__(2 * sizeof(S)) TK {
   S t, k;
 };
 
+// What a tile stages per node.  Two-knot laws (LIN) and TI runs stage T alone:
+// k is linear between the knots, so an element's mean conductivity is k(mean
+// T) unless a staged temperature lies outside them (`kclamp`, tile-uniform,
+// found while staging; then the corner values are interpolated one by one).
+// Laws with more knots (KST) stage (T, k(T)) pairs.
+template <typename S, bool KST>
+using Staged = std::conditional_t<KST, TK<S>, S>;
+template <typename S>
+__device__ __forceinline__ S st_T(const S *sT, int i) { return sT[i]; }
+template <typename S>
+__device__ __forceinline__ S st_T(const TK<S> *sT, int i) { return sT[i].t; }
+
 // products that must not be contracted into an FMA (keeps T == Ta a bitwise
 // fixed point: kb*T and qb = kb*Ta round identically)
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
@@ -154,6 +166,24 @@ __device__ __forceinline__ S kbar_from(const Curve<S> &kc, const S *Tn, int n, S
   for (int b = 0; b < 8; ++b)
     if (b < n) s += ip<LIN>(kc, Tn[b]);
   return s / S(n) * kf;
+}
+
+// material-0 mean conductivity of a slot from its corner temperatures (two-knot law kc)
+template <typename S, int N>
+__device__ __forceinline__ S kbar_lin(const Curve<S> &kc, const S (&T)[N], bool kclamp, S kf) {
+  if (!kclamp) {
+    S sum;
+    if constexpr (N == 8) sum = ((T[0] + T[1]) + (T[2] + T[3])) + ((T[4] + T[5]) + (T[6] + T[7]));
+    else sum = (T[0] + T[1]) + (T[2] + T[3]);
+    return (kc.slope[0] * (sum * S(1.0 / N) - kc.x[0]) + kc.y[0]) * kf;
+  }
+  S K[N];
+#pragma unroll
+  for (int b = 0; b < N; ++b) K[b] = ip<true>(kc, T[b]);
+  S sum;
+  if constexpr (N == 8) sum = ((K[0] + K[1]) + (K[2] + K[3])) + ((K[4] + K[5]) + (K[6] + K[7]));
+  else sum = (K[0] + K[1]) + (K[2] + K[3]);
+  return sum * S(1.0 / N) * kf;
 }
 
 __device__ __forceinline__ float fast_div(float a, float b) { return __fdividef(a, b); }
@@ -265,8 +295,10 @@ __device__ __forceinline__ void lean_issue(const TiledArgs<S> &g, int s_start, i
 
 // element loads of staged slot i of the batch ------------------------------------
 template <typename S, bool TD, bool LIN>
-__device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned char *stage, const TK<S> *sT,
-                                          int reg, bool has_kf, int i, uint16_t nd[8], S c[8]) {
+__device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned char *stage,
+                                          const Staged<S, TD && !LIN> *sT, bool kclamp, int reg, bool has_kf, int i,
+                                          uint16_t nd[8], S c[8]) {
+  constexpr bool KST = TD && !LIN;
   const StageLayout<S> L(8, has_kf, g.hex_rank != nullptr, g.hex_region != nullptr);
   const uint4 w = reinterpret_cast<const uint4 *>(stage + L.conn)[i];
   nd[0] = w.x & 0xffff; nd[1] = w.x >> 16; nd[2] = w.y & 0xffff; nd[3] = w.y >> 16;
@@ -274,9 +306,14 @@ __device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned 
   S T[8], K[8];
 #pragma unroll
   for (int b = 0; b < 8; ++b) {
-    const TK<S> q = sT[nd[b]];
-    T[b] = q.t;
-    K[b] = q.k;
+    if constexpr (KST) {
+      const TK<S> q = sT[nd[b]];
+      T[b] = q.t;
+      K[b] = q.k;
+    } else {
+      T[b] = sT[nd[b]];
+      K[b] = S(0);
+    }
   }
   const S *G = reinterpret_cast<const S *>(stage + L.G);
   const S g00 = G[i], g01 = G[kBatch + i], g02 = G[2 * kBatch + i], g11 = G[3 * kBatch + i],
@@ -284,7 +321,9 @@ __device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned 
   const S kf = has_kf ? reinterpret_cast<const S *>(stage + L.kf)[i] : S(1);
   S kb = kf;
   if (TD) {
-    if (reg == 0) {  // k(T) of material 0 staged per node: kbar = mean of the corner values
+    if (reg == 0 && !KST) {  // two-knot law of material 0
+      kb = kbar_lin<S, 8>(g.mats.m[0].k, T, kclamp, kf);
+    } else if (reg == 0) {  // k(T) of material 0 staged per node: kbar = mean of the corner values
       const S sum = ((K[0] + K[1]) + (K[2] + K[3])) + ((K[4] + K[5]) + (K[6] + K[7]));
       kb = sum * S(0.125) * kf;
     } else {  // other materials (rare slots): the element's own curve at each corner
@@ -307,9 +346,10 @@ __device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned 
 // with accumulator rows (g.tet_rows > 1) each 16-bit word is row << 14 | local
 // index; rofs[a] = row * row_stride locates the corner's accumulator
 template <typename S, bool TD, bool LIN>
-__device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned char *stage, const TK<S> *sT,
-                                          int reg, bool has_kf, int i, uint16_t nd[4], S c[4], int rofs[4],
-                                          uint32_t idx_mask, int row_stride) {
+__device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned char *stage,
+                                          const Staged<S, TD && !LIN> *sT, bool kclamp, int reg, bool has_kf, int i,
+                                          uint16_t nd[4], S c[4], int rofs[4], uint32_t idx_mask, int row_stride) {
+  constexpr bool KST = TD && !LIN;
   const StageLayout<S> L(4, has_kf, g.tet_rank != nullptr, g.tet_region != nullptr);
   const uint2 w = reinterpret_cast<const uint2 *>(stage + L.conn)[i];
   const uint32_t raw[4] = {w.x & 0xffffu, w.x >> 16, w.y & 0xffffu, w.y >> 16};
@@ -321,9 +361,14 @@ __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned 
   S T[4], K[4];
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
-    const TK<S> q = sT[nd[b]];
-    T[b] = q.t;
-    K[b] = q.k;
+    if constexpr (KST) {
+      const TK<S> q = sT[nd[b]];
+      T[b] = q.t;
+      K[b] = q.k;
+    } else {
+      T[b] = sT[nd[b]];
+      K[b] = S(0);
+    }
   }
   const S *G = reinterpret_cast<const S *>(stage + L.G);
   const S g00 = G[i], g01 = G[kBatch + i], g02 = G[2 * kBatch + i], g11 = G[3 * kBatch + i],
@@ -331,7 +376,9 @@ __device__ __forceinline__ void tet_loads(const TiledArgs<S> &g, const unsigned 
   const S kf = has_kf ? reinterpret_cast<const S *>(stage + L.kf)[i] : S(1);
   S kb = kf;
   if (TD) {
-    if (reg == 0) {
+    if (reg == 0 && !KST) {
+      kb = kbar_lin<S, 4>(g.mats.m[0].k, T, kclamp, kf);
+    } else if (reg == 0) {
       kb = ((K[0] + K[1]) + (K[2] + K[3])) * S(0.25) * kf;
     } else {
       kb = kbar_from<LIN>(g.mats.m[reg].k, T, 4, kf);
@@ -455,7 +502,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
                                                                 : (KINDS == 1 ? kMinBlocksTetF64 : 2))
     k_tiled_step(const __grid_constant__ TiledArgs<S> g) {
   extern __shared__ __align__(128) unsigned char smem[];
-  TK<S> *sT = reinterpret_cast<TK<S> *>(smem);
+  constexpr bool KST = TD && !LIN;  // stage (T, k(T)) pairs; otherwise T alone (see Staged)
+  using ST = Staged<S, KST>;
+  ST *sT = reinterpret_cast<ST *>(smem);
   S *acc = reinterpret_cast<S *>(smem + g.smem_T);
   unsigned char *ring = smem + g.smem_T + g.smem_acc;
   const int kStages = g.n_stages;
@@ -522,17 +571,20 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   }
   // stage temperatures: owned range + halo list; zero accumulators.  Loads
   // are clamped to valid addresses and only the shared stores are predicated,
-  // so the unrolled rounds stay branch-free; k(T) of material 0 comes from a
-  // two-knot law held in registers (LIN) -- other materials interpolate per slot.
-  const bool kstage = TD;
+  // so the unrolled rounds stay branch-free.  Two-knot laws stage T alone and
+  // note whether any staged temperature lies outside material 0's conductivity
+  // knots (kout -> kclamp); laws with more knots stage k(T) of material 0 too.
   const Curve<S> &k0 = g.mats.m[0].k;
-  const S kx0 = k0.x[0], kx1 = k0.x[1], ky0 = k0.y[0], ky1 = k0.y[1], ks = k0.slope[0];
-  auto k_of = [&](S x) -> S {
-    if (!kstage) return S(0);
-    if (!LIN) return interp(k0, x);
-    S r = ks * (x - kx0) + ky0;  // == ip<true>(k0, x), operation for operation
-    r = (x >= kx1) ? ky1 : r;
-    return (x <= kx0) ? ky0 : r;
+  const S kx0 = k0.x[0], kx1 = k0.x[1];
+  const bool ksloped = TD && LIN && k0.slope[0] != S(0);
+  bool kout = false;
+  auto staged = [&](S x) -> ST {
+    if constexpr (KST) {
+      return TK<S>{x, interp(k0, x)};
+    } else {
+      if (TD && LIN) kout |= (x < kx0) | (x > kx1);
+      return x;
+    }
   };
   // loads in flight per thread while staging (tet-only tiles: 4, measured
   // 1% faster on cfg3; hex tiles: 8)
@@ -544,7 +596,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = base + u * kTileThreads;
-      const TK<S> v{x[u], k_of(x[u])};
+      const ST v = staged(x[u]);
       if (i < nn) sT[i] = v;
     }
   }
@@ -562,12 +614,13 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = base + u * kTileThreads;
-      const TK<S> v{x[u], k_of(x[u])};
+      const ST v = staged(x[u]);
       if (i < nh) sT[nn + i] = v;
     }
   }
-  if (tid == 0) sT[nn + nh] = TK<S>{S(0), S(0)};  // the padding slots' dummy node (partition step 5)
-  __syncthreads();  // every halo id has been read: the accumulators may be zeroed
+  if (tid == 0) sT[nn + nh] = ST{};  // the padding slots' dummy node (partition step 5): T = 0
+  // every halo id has been read: the accumulators may be zeroed
+  const bool kclamp = __syncthreads_or(kout && ksloped) != 0;
   const int acc_rows = max(MODE == kCornerPhase2 ? 2 : 1,
                            KINDS == 2 ? 1 : g.tet_rows);
   for (int i = tid; i < acc_rows * nfree; i += kTileThreads) acc[i] = S(0);
@@ -638,15 +691,11 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
           nd[a] = (uint16_t)(raw[a] & 0x3fffu);
           rofs[a] = (int)(raw[a] >> 14) * nfree;
         }
-        S T[4], K[4];
+        S T[4];
 #pragma unroll
-        for (int b2 = 0; b2 < 4; ++b2) {
-          const TK<S> q = sT[nd[b2]];
-          T[b2] = q.t;
-          K[b2] = q.k;
-        }
+        for (int b2 = 0; b2 < 4; ++b2) T[b2] = sT[nd[b2]];
         // tet_loads with reg == 0 and kf == 1
-        const S kb = ((K[0] + K[1]) + (K[2] + K[3])) * S(0.25) * S(1);
+        const S kb = kbar_lin<S, 4>(k0, T, kclamp, S(1));
         const S d1 = T[1] - T[0], d2 = T[2] - T[0], d3 = T[3] - T[0];
         S c[4];
         c[1] = kb * (g00 * d1 + g01 * d2 + g02 * d3);
@@ -686,16 +735,11 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         uint16_t nd[kSPT][8];
         nd[0][0] = w.x & 0xffff; nd[0][1] = w.x >> 16; nd[0][2] = w.y & 0xffff; nd[0][3] = w.y >> 16;
         nd[0][4] = w.z & 0xffff; nd[0][5] = w.z >> 16; nd[0][6] = w.w & 0xffff; nd[0][7] = w.w >> 16;
-        S T[8], K[8];
+        S T[8];
 #pragma unroll
-        for (int b2 = 0; b2 < 8; ++b2) {
-          const TK<S> q = sT[nd[0][b2]];
-          T[b2] = q.t;
-          K[b2] = q.k;
-        }
+        for (int b2 = 0; b2 < 8; ++b2) T[b2] = sT[nd[0][b2]];
         // hex_loads with reg == 0 and kf == 1
-        const S sum = ((K[0] + K[1]) + (K[2] + K[3])) + ((K[4] + K[5]) + (K[6] + K[7]));
-        const S kb = sum * S(0.125) * S(1);
+        const S kb = kbar_lin<S, 8>(k0, T, kclamp, S(1));
         const S gx = ((T[1] - T[0]) + (T[2] - T[3])) + ((T[5] - T[4]) + (T[6] - T[7]));
         const S gy = ((T[3] - T[0]) + (T[2] - T[1])) + ((T[7] - T[4]) + (T[6] - T[5]));
         const S gz = ((T[4] - T[0]) + (T[5] - T[1])) + ((T[6] - T[2]) + (T[7] - T[3]));
@@ -749,7 +793,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         // instead of branching; only their accumulation is predicated off
         const int i = valid[q] ? q * kTileThreads + tid : 0;
         const int reg = t_reg ? (int)stage[Lt.region + i] : tile_reg;
-        tet_loads<S, TD, LIN>(g, stage, sT, reg, t_kf, i, nd[q], c[q], rofs[q], t_mask, nfree);
+        tet_loads<S, TD, LIN>(g, stage, sT, kclamp, reg, t_kf, i, nd[q], c[q], rofs[q], t_mask, nfree);
         FH_DEV_CHECK(nd[q][0] < nn + nh && nd[q][1] < nn + nh && nd[q][2] < nn + nh && nd[q][3] < nn + nh,
                      "tet corner outside the tile's staged nodes");
         // tets are never corner-unique: colour phases (phase byte per slot) or,
@@ -776,7 +820,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       for (int q = 0; q < kSPT; ++q) {
         const int i = valid[q] ? q * kTileThreads + tid : 0;
         const int reg = h_reg ? (int)stage[Lh.region + i] : tile_reg;
-        hex_loads<S, TD, LIN>(g, stage, sT, reg, h_kf, i, nd[q], c[q]);
+        hex_loads<S, TD, LIN>(g, stage, sT, kclamp, reg, h_kf, i, nd[q], c[q]);
 #ifdef FH_CHECKS
         for (int a = 0; a < 8; ++a) FH_DEV_CHECK(nd[q][a] < nn + nh, "hex corner outside the tile's staged nodes");
 #endif
@@ -855,7 +899,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         const bool ok = base + u * kTileThreads < nfree;
         const int loc = ok ? base + u * kTileThreads : 0;
         const int n = n0 + loc;
-        const S x = sT[loc].t;
+        const S x = st_T(sT, loc);
         S Fsum;
         if (MODE == kCornerPhase2) {
           Fsum = acc[loc] + acc[nfree + loc];

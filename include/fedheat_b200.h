@@ -158,7 +158,7 @@ typedef struct {
   int32_t resident_ctas;    /* resident path: CTA count (0: one per SM) */
   int32_t tile_mode;        /* TILED hex accumulation mode + 1 (0: default) */
   int32_t tile_stages;      /* TILED TMA ring depth (0: default 2) */
-  int32_t tet_rows;         /* TILED tet accumulator rows: 0 default, 1 or 4 */
+  int32_t tet_rows;         /* TILED tet accumulator rows: 0 default (4 on tet-only meshes), or 1..4 */
   int32_t launch_order;     /* TILED: 0 default, 1 partition (RCB) order, 2 longest tiles first */
   int32_t kind_split;       /* TILED mixed meshes: 0 default (split hex-only tiles), 1 one launch */
   int32_t hex_color;        /* TILED: 0 default, 1 colour-sort hex slots even when corner-unique */
@@ -166,6 +166,8 @@ typedef struct {
   int32_t allow_nondeterministic; /* must be 1 for tile_mode = shared-memory atomics (5) */
   int32_t lean_kernels;     /* TILED: 0 auto (specialised batch loops for tet-only colour / hex-only
                                two-row corner-phase tiles), 1 off (the general kernel) */
+  int32_t resident_sync;    /* resident path: 0 default (stamped halo words, no grid barrier; a runaway
+                               call is replayed up to the failing step), 1 grid barrier per step */
 } fh_options;
 
 typedef struct {

@@ -62,7 +62,8 @@ class FhBoundary(C.Structure):
 
 # fh_options tuning knobs (include/fedheat_b200.h); 0 = the measured default
 TUNING_FIELDS = ("exact_resident", "resident_ctas", "tile_mode", "tile_stages", "tet_rows", "launch_order",
-                 "kind_split", "hex_color", "first_touch", "allow_nondeterministic", "lean_kernels")
+                 "kind_split", "hex_color", "first_touch", "allow_nondeterministic", "lean_kernels",
+                 "resident_sync")
 
 
 class FhOptions(C.Structure):

@@ -241,6 +241,9 @@ struct fh_engine {
   DBuf<uint8_t> r_info;
   DBuf<double> T1;
   DBuf<unsigned long long> r_bar;
+  DBuf<unsigned long long> r_ll[2];  // stamped-word buffers of the resident kernel (2 words per node)
+  uint32_t r_epoch = 1;              // next unused stamp (0 = never written)
+  DBuf<double> r_snap;               // field at the start of a call (replay after a runaway)
   // ATOMIC assembly (fh_atomic.cu): element streams in the TILED numbering
   AtomicState atom;
   DBuf<int32_t> a_tet_conn, a_hex_conn;
@@ -343,10 +346,12 @@ int default_part_nodes(int precision, int64_t n_tet, int64_t n_hex) {
 }
 
 // Tet-only meshes: colour classes with up to 4 writes per node (4 accumulator
-// rows, ~4x larger classes -> fewer colour phases per 256-slot batch).
-int default_tet_rows(int64_t n_tet, int64_t n_hex, int knob) {
-  int r = (n_tet > 0 && n_hex == 0) ? 4 : 1;
-  if (knob > 0) r = knob > 1 ? 4 : 1;  // fh_options.tet_rows
+// rows, ~4x larger classes -> fewer colour phases per 256-slot batch).  fp64
+// keeps 3 rows: the row saved lets a fourth tile CTA fit each SM's shared
+// memory (cfg3 fp64 0.1068 -> 0.1000 ms/step; 2 rows 0.1008).
+int default_tet_rows(int64_t n_tet, int64_t n_hex, int knob, int precision) {
+  int r = (n_tet > 0 && n_hex == 0) ? (precision == 32 ? 4 : 3) : 1;
+  if (knob > 0) r = std::min(knob, 4);  // fh_options.tet_rows
   return r;
 }
 
@@ -364,7 +369,7 @@ int wave_fit_part_nodes(int target, int64_t V, int n_domains, int precision, int
   }
   // resident step CTAs per SM (the launch bounds of k_tiled_step)
   // (the launch bounds' minimum; setup_tiled refits with the measured value)
-  const int per_sm = per_sm_measured > 0 ? per_sm_measured : (precision != 32 ? 2 : (n_hex == 0 ? 5 : 4));
+  const int per_sm = per_sm_measured > 0 ? per_sm_measured : (precision != 32 ? 2 : (n_hex == 0 ? 6 : 5));
   const int64_t cap = (int64_t)sms * per_sm;
   const int64_t vd = (V + n_domains - 1) / n_domains;
   const int64_t n0 = (int64_t)n_domains * ((vd + target - 1) / target);
@@ -512,16 +517,28 @@ void setup_exact(fh_engine *e, const fh_boundary &b) {
 void setup_resident(fh_engine *e, const std::vector<int32_t> &conn, const std::vector<int32_t> &offs,
                     const std::vector<int32_t> &pos) {
   const fh_options &o = e->opts;
+  if (o.resident_sync < 0 || o.resident_sync > 1) fail(FH_ERR_CONFIG, "resident_sync must be 0 or 1");
   if (o.exact_resident == 1) return;
   int sms = 148, smem_optin = 227 * 1024;
   FH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
   FH_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
   const bool stage_k = e->td && !(o.n_materials > 1 && o.element_region);
-  const int ctas = o.resident_ctas > 0 ? o.resident_ctas : sms;
+  // CTA count: the knob, else two per SM with stamped halo words (measured:
+  // cfg1 2.39 -> 2.25 us/step, cfg2 3.56 -> 3.21 over one per SM; the grid
+  // barrier is fastest with one per SM), falling back to one per SM when two
+  // do not stay co-resident
+  std::vector<int> tries;
+  if (o.resident_ctas > 0) tries = {o.resident_ctas};
+  else if (o.resident_sync == 0) tries = {2 * sms, sms};
+  else tries = {sms};
   ResidentPlan P;
-  bool ok = build_resident_plan(e->V, e->n_tet, FH_CHUNK_SIZE, conn, offs, pos, ctas, stage_k, !e->td,
-                                (size_t)smem_optin - 1024, P);
-  if (ok) ok = (int64_t)resident_occupancy(e->td, stage_k, P.threads, P.smem) * sms >= P.n_cta;
+  bool ok = false;
+  for (int ctas : tries) {
+    ok = build_resident_plan(e->V, e->n_tet, FH_CHUNK_SIZE, conn, offs, pos, ctas, stage_k, !e->td,
+                             (size_t)smem_optin - 1024, P);
+    if (ok) ok = (int64_t)resident_occupancy(e->td, stage_k, P.threads, P.smem) * sms >= P.n_cta;
+    if (ok) break;
+  }
   if (!ok) {
     if (o.exact_resident == 2) fail(FH_ERR_CONFIG, "the resident EXACT path does not fit this mesh");
     return;
@@ -559,6 +576,14 @@ void setup_resident(fh_engine *e, const std::vector<int32_t> &conn, const std::v
   r.T0 = e->T.p;
   r.T1 = e->T1.p;
   r.bar = e->r_bar.p;
+  if (o.resident_sync != 1) {  // stamped halo words instead of a grid barrier per step
+    for (int q = 0; q < 2; ++q) {
+      e->r_ll[q].alloc(2 * (size_t)e->V);
+      e->r_ll[q].zero(s);
+      r.ll[q] = e->r_ll[q].p;
+    }
+    e->r_snap.alloc(e->V);
+  }
   e->resident = true;
   e->res_stage_k = stage_k;
   e->res_ctas = P.n_cta;
@@ -598,7 +623,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   // layout tuning knobs (fh_options; scripts/sweep.py): hex colour order, first-touch node order
   pin.hex_color = o.hex_color;
   pin.first_touch = o.first_touch;
-  pin.tet_rows = default_tet_rows(e->n_tet, e->n_hex, o.tet_rows);
+  pin.tet_rows = default_tet_rows(e->n_tet, e->n_hex, o.tet_rows, sizeof(S) == 4 ? 32 : 64);
   pin.n_domains = std::max(1, o.n_domains);
   pin.slab_axis = o.slab_axis;
   build_partition(pin, e->part);
@@ -643,7 +668,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     sms = 148;
   }
   const int per_sm = e->refit_per_sm > 0 ? e->refit_per_sm
-                                         : (sizeof(S) == 4 ? (e->n_hex == 0 ? 5 : 4) : 2);
+                                         : (sizeof(S) == 4 ? (e->n_hex == 0 ? 6 : 5) : 2);
   bool lpt = (double)plist.size() / ((double)sms * per_sm) < 6.0;
   if (o.launch_order) lpt = o.launch_order == 2;
   if (lpt) {
@@ -799,7 +824,7 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     int max_b = 0;
     for (int q = 0; q < P.n_parts; ++q)
       max_b = std::max(max_b, (P.part_tet_count[q] + kBatch - 1) / kBatch + (P.part_hex_count[q] + kBatch - 1) / kBatch);
-    const bool kind_ok = nhs == 0 ? (tet_mode == kModeColored && P.tet_rows == 4)
+    const bool kind_ok = nhs == 0 ? (tet_mode == kModeColored && P.tet_rows >= 2)
                                   : (nts == 0 && mode == kModeCornerPhase2);
     st->lean = e->td && lin_ok && o.lean_kernels == 0 && !regions &&
                !st->tet_kf.p && !st->hex_kf.p && kind_ok && max_b <= kBatch;
@@ -1279,12 +1304,22 @@ void resident_exact_run(fh_engine *e, int64_t nsteps, double dt) {
       exact_props(e->ex, e->T.p, e->stream);
       e->frozen = true;
     }
-    int64_t seg = nsteps - k;
+    int64_t seg = std::min<int64_t>(nsteps - k, (int64_t)1 << 30);
     if (!e->load_power.empty()) {
       seg = 1;
-      while (k + seg < nsteps && !loads_differ_at(e, (double)(e->step_index + seg) * dt)) ++seg;
+      while (k + seg < nsteps && seg < ((int64_t)1 << 30) && !loads_differ_at(e, (double)(e->step_index + seg) * dt))
+        ++seg;
     }
     ResidentArgs r = e->res;
+    if (r.ll[0]) {  // this launch's stamps: [epoch, epoch + seg]; never reused before the buffers are cleared
+      if ((uint64_t)e->r_epoch + (uint64_t)seg + 1 >= 0xffffffffull) {
+        e->r_ll[0].zero(e->stream);
+        e->r_ll[1].zero(e->stream);
+        e->r_epoch = 1;
+      }
+      r.stamp0 = e->r_epoch;
+      e->r_epoch += (uint32_t)seg + 1u;
+    }
     r.g = e->ex;
     r.step0 = e->step_index;
     r.nsteps = seg;
@@ -1433,6 +1468,14 @@ int do_step(fh_engine *e, int64_t nsteps, double dt, fh_report *rep, float *elap
       snapshot_T<double>(e, false);
     }
   }
+  // resident EXACT kernel without a grid barrier: a runaway is only recorded
+  // while the launch runs on, so the call is replayed from its start for
+  // exactly the steps up to the failing one (deterministic; the field is then
+  // the one right after that step, as on the two-launch path)
+  const bool res_replay = e->assembly == FH_ASSEMBLY_EXACT && e->resident && !e->dir_runaway && e->res.ll[0];
+  const bool frozen0 = e->frozen;
+  if (res_replay)
+    FH_CUDA(cudaMemcpyAsync(e->r_snap.p, e->T.p, sizeof(double) * (size_t)e->V, cudaMemcpyDeviceToDevice, e->stream));
   if (scratch) {
     sev.resize(2 * nsteps);
     for (auto &v : sev) FH_CUDA(cudaEventCreate(&v));
@@ -1505,6 +1548,27 @@ int do_step(fh_engine *e, int64_t nsteps, double dt, fh_report *rep, float *elap
         rank_min_u64(e, f1.step);
         FH_CUDA(cudaMemcpyAsync(e->flag.p, &f1, sizeof(f1), cudaMemcpyHostToDevice, e->stream));
       }
+    }
+  }
+  if (res_replay) {
+    FailFlag fr{};
+    unsigned long long lost = 0;
+    FH_CUDA(cudaMemcpyAsync(&fr, e->flag.p, sizeof(fr), cudaMemcpyDeviceToHost, e->stream));
+    FH_CUDA(cudaMemcpyAsync(&lost, e->r_bar.p, sizeof(lost), cudaMemcpyDeviceToHost, e->stream));
+    FH_CUDA(cudaStreamSynchronize(e->stream));
+    if (lost) fail(FH_ERR_DEVICE, "resident kernel: a CTA stopped receiving its neighbours' temperatures");
+    if (fr.step != ~0ull && (int64_t)fr.step > step0) {
+      const int64_t fs = (int64_t)fr.step;
+      const FailFlag clear{~0ull};
+      FH_CUDA(cudaMemcpyAsync(e->flag.p, &clear, sizeof(clear), cudaMemcpyHostToDevice, e->stream));
+      FH_CUDA(cudaMemcpyAsync(e->T.p, e->r_snap.p, sizeof(double) * (size_t)e->V, cudaMemcpyDeviceToDevice, e->stream));
+      e->step_index = step0;
+      e->time = time0;
+      e->n_rec = nrec0;
+      e->probe_steps.resize(nps0);
+      e->qr_valid = false;
+      e->frozen = frozen0;
+      run_steps(e, fs - step0, dt);  // its last step fails again and sets the flag to fs
     }
   }
   if (elapsed_ms && !scratch) {
@@ -2474,7 +2538,7 @@ int fh_plan_create(const fh_mesh *mesh, const fh_boundary *bnd, const fh_options
   // layout tuning knobs (fh_options): hex colour order, first-touch node order
   pin.hex_color = opts->hex_color;
   pin.first_touch = opts->first_touch;
-  pin.tet_rows = default_tet_rows(mesh->n_tets, mesh->n_hexes, opts->tet_rows);
+  pin.tet_rows = default_tet_rows(mesh->n_tets, mesh->n_hexes, opts->tet_rows, opts->precision);
   pin.n_domains = std::max(1, opts->n_domains);
   pin.slab_axis = opts->slab_axis;
   build_partition(pin, pl->P);

@@ -15,9 +15,16 @@
 //     owned node's incidences in chunk order (kernels.py:113-134), run the
 //     lumped update, the Dirichlet overwrite and the runaway check
 //     (kernels.py:137-142, solver.py:354-382) and write the other buffer;
-//   * a grid barrier ends the step; every CTA then reads the fail flag, so the
-//     failing step completes and nothing after it runs (the state is the one
-//     right after that step, like the two-launch path).
+//   * between steps the CTAs synchronise either through a grid barrier
+//     (SYNC_BARRIER: every CTA then reads the fail flag, so the failing step
+//     completes and nothing after it runs) or -- the default -- not at all:
+//     every new temperature is published as two 8-byte words that each carry
+//     half of the value and the step's stamp, and a CTA starts its next step
+//     as soon as the stamped values of ITS halo nodes have arrived
+//     (SYNC_STAMPED: one L2 round trip per step instead of a release / arrive /
+//     poll / reload chain).  A runaway is then only recorded; the host replays
+//     the launch up to the failing step (deterministic), which leaves the
+//     field right after that step like the two-launch path.
 //
 // The arithmetic is the EXACT path's (fh_exact_dev.cuh, -fmad=false, explicit
 // _rn intrinsics in the reference's order), so the fields are bit-identical
@@ -62,7 +69,37 @@ __device__ __forceinline__ bool grid_barrier(unsigned long long *bar, unsigned l
   return (*s_word >> 40) != 0;
 }
 
-template <bool TD, bool KSTAGE>
+// Stamped words (the LL idea of collective libraries): 8-byte stores are single
+// copy atomic, so {32 value bits, 32 stamp bits} arrives whole; a double is two
+// such words and is complete when both carry the expected stamp.  The stamps
+// of a launch are stamp0 + (steps taken in it) and never repeat across
+// launches (the host hands out stamp0 from a 32-bit epoch and clears the
+// buffers before it wraps), so a stale word is never mistaken for a new one.
+__device__ __forceinline__ void st_stamped(unsigned long long *slot, double x, uint32_t stamp) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  const unsigned long long hi = (unsigned long long)stamp << 32;
+  const unsigned long long w0 = (b & 0xffffffffull) | hi, w1 = (b >> 32) | hi;
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(slot), "l"(w0), "l"(w1) : "memory");
+}
+// spins until both words carry `stamp`.  Gives up (false) after ~2^22 polls or
+// as soon as another CTA gave up (*lost != 0): the launch then ends and the
+// host reports an internal error instead of hanging the device.
+__device__ __forceinline__ bool ld_stamped(const unsigned long long *slot, uint32_t stamp, double &x,
+                                           unsigned long long *lost) {
+  for (int spin = 1; spin <= (1 << 22); ++spin) {
+    unsigned long long w0, w1;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(slot) : "memory");
+    if ((uint32_t)(w0 >> 32) == stamp && (uint32_t)(w1 >> 32) == stamp) {
+      x = __longlong_as_double((long long)((w0 & 0xffffffffull) | (w1 << 32)));
+      return true;
+    }
+    if ((spin & 1023) == 0 && *reinterpret_cast<volatile unsigned long long *>(lost) != 0ull) break;
+  }
+  atomicExch(lost, 1ull);
+  return false;
+}
+
+template <bool TD, bool KSTAGE, bool STAMPED>
 __global__ void __launch_bounds__(kResThreads, 1) k_resident(const __grid_constant__ ResidentArgs r) {
   const ExactArgs &g = r.g;
   // an earlier call's step failed: every later launch is a no-op (fh_step semantics)
@@ -112,6 +149,14 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(const __grid_consta
 
   const Curve<double> &k0 = g.mats.m[0].k;
   int64_t done = r.nsteps;
+  if (STAMPED) {
+    // publish the owned nodes of the field as given (stamp of step 0 of this launch)
+    for (int i = tid; i < nown; i += bd) {
+      const double x = __ldcg(r.T0 + n0 + i);
+      sT[i] = x;
+      st_stamped(r.ll[0] + 2 * (size_t)(n0 + i), x, r.stamp0);
+    }
+  }
   for (int64_t j = 0; j < r.nsteps; ++j) {
     const double *Tc = (j & 1) ? r.T1 : r.T0;
     double *Tn = (j & 1) ? r.T0 : r.T1;
@@ -119,14 +164,35 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(const __grid_consta
     const double t = j == 0 ? r.time0 : (double)(r.step0 + j) * r.dt;
     // 1. temperatures (and k(T), single material) of the owned + halo nodes;
     //    written by other CTAs in the previous step: L2 loads (no stale L1)
-    for (int i = tid; i < nloc; i += bd) {
-      const int gi = i < nown ? n0 + i : sH[i - nown];
-      FH_DEV_CHECK(gi >= 0 && gi < g.V, "resident staged node");
-      const double x = __ldcg(Tc + gi);
-      sT[i] = x;
-      if (TD && KSTAGE) sK[i] = interp_rn(k0, x);
+    if (STAMPED) {
+      // the owned nodes are in sT already (the previous step's update); the
+      // halo nodes arrive as stamped words from their owners.  A slot of
+      // buffer j & 1 is rewritten by its owner in step j + 1, which the owner
+      // starts only after every reader's step-j output (stamped after its reads) arrived.
+      const unsigned long long *src = r.ll[j & 1];
+      const uint32_t stamp = r.stamp0 + (uint32_t)j;
+      for (int i = tid; i < nloc; i += bd) {
+        double x;
+        if (i < nown) {
+          x = sT[i];
+        } else if (!ld_stamped(src + 2 * (size_t)sH[i - nown], stamp, x, r.bar)) {
+          s_bad = 2;  // lost a neighbour: this CTA leaves after the staging barrier
+          x = 0.0;
+        }
+        if (i >= nown) sT[i] = x;
+        if (TD && KSTAGE) sK[i] = interp_rn(k0, x);
+      }
+    } else {
+      for (int i = tid; i < nloc; i += bd) {
+        const int gi = i < nown ? n0 + i : sH[i - nown];
+        FH_DEV_CHECK(gi >= 0 && gi < g.V, "resident staged node");
+        const double x = __ldcg(Tc + gi);
+        sT[i] = x;
+        if (TD && KSTAGE) sK[i] = interp_rn(k0, x);
+      }
     }
     __syncthreads();
+    if (STAMPED && s_bad == 2) return;
     // 2. one contribution per incidence (k_exact_elem's arithmetic): the
     //    corner loads, differences and products are independent, only the
     //    sum runs in the reference's b order
@@ -228,13 +294,14 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(const __grid_consta
       const int gi = n0 + i;
       if (g.F) g.F[gi] = total;
       const double xn = exact_update_in(g, sN[i], total, sT[i], r.dt, t, TD ? 1 : 0);
-      Tn[gi] = xn;
-      sT[i] = xn;  // the probes below read the owned nodes' new values
+      if (STAMPED) st_stamped(r.ll[(j + 1) & 1] + 2 * (size_t)gi, xn, r.stamp0 + (uint32_t)j + 1u);
+      else Tn[gi] = xn;
+      sT[i] = xn;  // the next step and the probes below read the owned nodes' new values
       bad |= !isfinite(xn) || fabs(xn) > g.runaway_limit;
     }
     if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) {
       atomicMin(&g.flag->step, step_no);
-      s_bad = 1;
+      if (!STAMPED) s_bad = 1;
     }
     // probe record of this step, written by the CTA owning each probe node
     // (k_gather_probes' values; a failing step's record is dropped by the host)
@@ -249,19 +316,30 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(const __grid_consta
         }
       }
     }
+    if (STAMPED) {
+      // no barrier: sT's owned entries are next read after the staging barrier
+      // of the next step, its halo entries and sK only rewritten before it
+      continue;
+    }
     if (grid_barrier(r.bar, (unsigned long long)(j + 1) * gridDim.x, s_bad != 0, &s_word)) {
       done = j + 1;  // this step failed somewhere: its field is complete, stop here
       break;
     }
+  }
+  if (STAMPED) {
+    // the engine's field: every CTA's owned nodes after the last step
+    __syncthreads();
+    for (int i = tid; i < nown; i += bd) r.T0[n0 + i] = sT[i];
+    return;
   }
   // the field after the last completed step is in T1 when that count is odd
   if (done & 1)
     for (int i = tid; i < nown; i += bd) r.T0[n0 + i] = __ldcg(r.T1 + n0 + i);
 }
 
-template <bool TD, bool KSTAGE>
+template <bool TD, bool KSTAGE, bool STAMPED>
 static void launch_one(const ResidentArgs &r, int n_cta, int threads, size_t smem, cudaStream_t s) {
-  auto kern = k_resident<TD, KSTAGE>;
+  auto kern = k_resident<TD, KSTAGE, STAMPED>;
   static size_t configured = 0;
   if (smem > configured) {
     FH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -274,18 +352,29 @@ static void launch_one(const ResidentArgs &r, int n_cta, int threads, size_t sme
 void resident_run(const ResidentArgs &r, int n_cta, int threads, size_t smem, bool td, bool stage_k,
                   cudaStream_t s) {
   if (r.nsteps <= 0) return;
-  if (td && stage_k) launch_one<true, true>(r, n_cta, threads, smem, s);
-  else if (td) launch_one<true, false>(r, n_cta, threads, smem, s);
-  else launch_one<false, false>(r, n_cta, threads, smem, s);
+  if (r.ll[0]) {
+    if (td && stage_k) launch_one<true, true, true>(r, n_cta, threads, smem, s);
+    else if (td) launch_one<true, false, true>(r, n_cta, threads, smem, s);
+    else launch_one<false, false, true>(r, n_cta, threads, smem, s);
+    return;
+  }
+  if (td && stage_k) launch_one<true, true, false>(r, n_cta, threads, smem, s);
+  else if (td) launch_one<true, false, false>(r, n_cta, threads, smem, s);
+  else launch_one<false, false, false>(r, n_cta, threads, smem, s);
 }
 
 template <bool TD, bool KSTAGE>
 static int occ_one(int threads, size_t smem) {
-  auto kern = k_resident<TD, KSTAGE>;
+  // both synchronisation variants of a (TD, KSTAGE) pair: the smaller count decides
+  auto kern2 = k_resident<TD, KSTAGE, true>;
+  FH_CUDA(cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int bps2 = 0;
+  FH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps2, kern2, threads, smem));
+  auto kern = k_resident<TD, KSTAGE, false>;
   FH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int bps = 0;
   FH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, threads, smem));
-  return bps;
+  return std::min(bps, bps2);
 }
 
 int resident_occupancy(bool td, bool stage_k, int threads, size_t smem) {

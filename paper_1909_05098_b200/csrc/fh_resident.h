@@ -40,7 +40,11 @@ struct ResidentArgs {
   const uint8_t *inc_info;
   uint32_t off_K, off_A, off_C, off_Kb, off_L, off_E, off_I, off_H, off_N, off_O;
   double *T0, *T1;        // T0: the engine's field (in and out), T1: ping-pong scratch
-  unsigned long long *bar;  // grid barrier word, zeroed before every launch
+  unsigned long long *bar;  // grid barrier word (stamped mode: set to 1 by a CTA that lost its neighbours), zeroed before every launch
+  // stamped mode (null: grid barrier): two buffers of 2 words per node, {value half | stamp << 32};
+  // the field at the start of step j of the launch carries stamp0 + j in ll[j & 1]
+  unsigned long long *ll[2];
+  uint32_t stamp0;
   int64_t step0;          // steps taken before this launch
   int64_t nsteps;
   double time0, dt;       // start time of the first step; later steps start at (step0 + j) * dt

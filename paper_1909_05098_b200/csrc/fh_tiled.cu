@@ -30,12 +30,14 @@ constexpr unsigned long long kNone = ~0ull;
 
 // minimum resident CTAs per SM requested from ptxas for the fp32 step kernel
 // (caps registers; the default is the measured best, see scripts/sweep.py)
+// (5 since the tiles stage T alone: 48 registers without spills and ~43 KB of
+// shared memory per 1536-node tile; cfg4 0.2623 -> 0.2484 ms/step over 4)
 #ifndef FH_MIN_BLOCKS_F32
-#define FH_MIN_BLOCKS_F32 4
+#define FH_MIN_BLOCKS_F32 5
 #endif
 constexpr int kMinBlocksF32 = FH_MIN_BLOCKS_F32;
 #ifndef FH_MIN_BLOCKS_TET
-#define FH_MIN_BLOCKS_TET 5
+#define FH_MIN_BLOCKS_TET 6
 #endif
 constexpr int kMinBlocksTet = FH_MIN_BLOCKS_TET;  // tet-only fp32 kernels: smaller tiles, more CTAs
 // tet-only fp64 kernels: 3 resident CTAs (<= 80 registers; cfg3 fp64 runs 4 waves of 3 CTAs/SM)
@@ -687,7 +689,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         uint16_t nd[4];
         int rofs[4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {  // LEAN tets always carry 4 accumulator rows (host condition)
+        for (int a = 0; a < 4; ++a) {  // LEAN tets always carry row-tagged connectivity (host condition)
           nd[a] = (uint16_t)(raw[a] & 0x3fffu);
           rofs[a] = (int)(raw[a] >> 14) * nfree;
         }
@@ -904,7 +906,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         if (MODE == kCornerPhase2) {
           Fsum = acc[loc] + acc[nfree + loc];
         } else if (KINDS == 1 && g.tet_rows > 1) {  // tet accumulator rows, summed in row order
-          Fsum = (acc[loc] + acc[nfree + loc]) + (acc[2 * nfree + loc] + acc[3 * nfree + loc]);
+          const S r01 = acc[loc] + acc[nfree + loc];
+          Fsum = g.tet_rows == 4   ? r01 + (acc[2 * nfree + loc] + acc[3 * nfree + loc])
+                 : g.tet_rows == 3 ? r01 + acc[2 * nfree + loc]
+                                   : r01;
         } else {
           Fsum = acc[loc];
         }

@@ -19,8 +19,8 @@ steps = int(sys.argv[2]) if len(sys.argv) > 2 else 1000
 prob = bench.make_problem(cfg, 0, 64)
 scratch = torch.empty(2 * 126 * 2**20, dtype=torch.uint8, device="cuda")
 ref = None
-for tun in ({"exact_resident": 1}, {}, {"resident_ctas": 16}, {"resident_ctas": 32}, {"resident_ctas": 64},
-            {"resident_ctas": 96}, {"resident_ctas": 296}):
+for tun in ({"exact_resident": 1}, {}, {"resident_sync": 1}, {"resident_ctas": 148}, {"resident_ctas": 222},
+            {"resident_ctas": 296}, {"resident_ctas": 444}, {"resident_ctas": 592}):
     kw = prob.engine_kwargs()
     kw["precision"] = 64
     try:

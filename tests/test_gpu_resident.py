@@ -1,5 +1,6 @@
 """The resident small-mesh EXACT path (csrc/fh_resident.cu): many steps per
-cooperative launch, one grid barrier per step.
+cooperative launch; the CTAs synchronise through stamped halo words (the
+default, ``resident_sync=0``) or a grid barrier per step (``resident_sync=1``).
 
 It must be bit-identical to the two-launch EXACT path (and so to the
 reference): every run below is done twice, once with the resident kernel
@@ -9,7 +10,8 @@ and fields, probes, inflow and failure reports are compared bit for bit.  The
 golden reference runs (tests/test_gpu_parity.py) already go through the
 resident kernel by default; these cases add the extensions, load windows that
 split a call into several launches, probe records across calls, TI freezing,
-instability and the step() API.
+instability and the step() API.  Every case runs in both synchronisation
+modes (the ``sync`` fixture).
 """
 
 import numpy as np
@@ -23,8 +25,18 @@ from paper_1909_05098_b200 import configs  # noqa: E402
 from golden_io import load, material  # noqa: E402
 
 
+@pytest.fixture(params=[0, 1], ids=["stamped", "barrier"], autouse=True)
+def sync(request):
+    global SYNC
+    SYNC = request.param
+    return request.param
+
+
+SYNC = 0
+
+
 def engines(mesh, mat, bnd=None, **kw):
-    res = fh.ExplicitEngine(mesh, mat, bnd, **kw)
+    res = fh.ExplicitEngine(mesh, mat, bnd, tuning={"resident_sync": SYNC}, **kw)
     two = fh.ExplicitEngine(mesh, mat, bnd, tuning={"exact_resident": 1}, **kw)
     assert res.layout()["resident_ctas"] > 0 and res.layout()["kernels_per_step"] == 0
     assert two.layout()["resident_ctas"] == 0 and two.layout()["kernels_per_step"] == 2
@@ -43,7 +55,8 @@ def test_golden_cfg2_resident_bitwise():
     from test_gpu_parity import golden_problem
 
     mesh, bnd = golden_problem(d)
-    eng = fh.ExplicitEngine(mesh, material(d), bnd, td_mode=bool(d["td_mode"]), tuning={"exact_resident": 2})
+    eng = fh.ExplicitEngine(mesh, material(d), bnd, td_mode=bool(d["td_mode"]),
+                            tuning={"exact_resident": 2, "resident_sync": SYNC})
     res = eng.run(d["T0"], steps=int(d["steps"]), dt=float(d["dt"]), probes=d["probes"],
                   probe_interval=int(d["interval"]))
     assert np.array_equal(res.state.temperatures, d["T_final"])
@@ -127,3 +140,24 @@ def test_instability_report_bitwise(td):
     assert errs[0].step == errs[1].step > 2
     assert errs[0].node == errs[1].node
     assert np.array_equal(a.temperature(), b.temperature())
+    # the engines stay usable: the same call fails the same way again, and a stable run follows
+    with pytest.raises(fh.InstabilityError) as again:
+        a.run(T0, steps=400, dt=dt)
+    assert again.value.step == errs[0].step and again.value.node == errs[0].node
+    ok_dt = 0.5 * a.critical_dt(T0)
+    same_run(a.run(T0, steps=30, dt=ok_dt), b.run(T0, steps=30, dt=ok_dt))
+
+
+def test_many_short_calls_keep_stamps_apart():
+    """Stamps never repeat across launches: many 1- and 2-step calls with state
+    resets in between (the step index restarts at 0 each time) stay bitwise."""
+    mesh = fh.generate_cube_mesh("hex", 10, 0.1)
+    mat = configs.pennes_td()
+    bnd = fh.BoundarySpec(dirichlet=(("x0", 37.0),), heat_loads=(("center", 0.5, 0.0, 1e9),))
+    a, b = engines(mesh, mat, bnd)
+    dt = 0.9 * a.critical_dt(37.0)
+    rng = np.random.default_rng(11)
+    for k in range(12):
+        T0 = 37.0 + rng.uniform(-0.5, 0.5, mesh.n_nodes)
+        n = 1 + k % 3
+        same_run(a.run(T0, steps=n, dt=dt), b.run(T0, steps=n, dt=dt))

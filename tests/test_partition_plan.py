@@ -160,9 +160,9 @@ def test_domain_range_validation():
 
 def test_wave_fit_default_tile_count():
     """With default part_nodes and fewer than 6 waves of resident CTAs, the
-    tile count is raised to fill the last wave (148 SMs x 5 tet CTAs = 740):
-    70^3 Kuhn tets, 8 domains -> 736 tiles instead of 472 at 768-node tiles."""
+    tile count is raised to fill the last wave (148 SMs x 6 tet CTAs = 888):
+    70^3 Kuhn tets, 8 domains -> 888 tiles instead of 472 at 768-node tiles."""
     mesh = fh.generate_cube_mesh("tet", 70, 0.1)
     info = Plan(mesh, MAT, n_domains=8).info
-    assert info["n_parts"] == 736
+    assert info["n_parts"] == 888
     assert Plan(mesh, MAT, n_domains=8, part_nodes=768).info["n_parts"] == 472

@@ -160,6 +160,16 @@ __global__ void k_pack_slots(const int32_t *__restrict__ slot_elem, int64_t n, c
   if (out_region) out_region[s] = e >= 0 ? (uint8_t)region[e] : 0;
 }
 
+// fp32 LEAN 1 records: the 16-bit node references become byte offsets (x 4;
+// tets keep their accumulator row in bits 14-15), see k_tiled_step
+__global__ void k_scale_conn(unsigned char *rec, int64_t n_batches, int rec_bytes, int words_per_batch, int tagged) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_batches * words_per_batch) return;
+  uint16_t *w = reinterpret_cast<uint16_t *>(rec + (i / words_per_batch) * rec_bytes) + i % words_per_batch;
+  const uint16_t v = *w;
+  *w = tagged ? (uint16_t)((v & 0xc000u) | ((v & 0x3fffu) << 2)) : (uint16_t)(v << 2);
+}
+
 constexpr int kBlk = 256;
 inline unsigned nblk(int64_t n) { return (unsigned)((n + kBlk - 1) / kBlk); }
 
@@ -826,8 +836,16 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
       max_b = std::max(max_b, (P.part_tet_count[q] + kBatch - 1) / kBatch + (P.part_hex_count[q] + kBatch - 1) / kBatch);
     const bool kind_ok = nhs == 0 ? (tet_mode == kModeColored && P.tet_rows >= 2)
                                   : (nts == 0 && mode == kModeCornerPhase2);
+    // fp32 LEAN records hold byte offsets in 16 (hex) / 14 (tets) bits
+    const bool offs_ok = sizeof(S) != 4 || 4 * ((int64_t)P.max_local_nodes + 1) <= (nhs == 0 ? 0x3fff : 0xffff);
     st->lean = e->td && lin_ok && o.lean_kernels == 0 && !regions &&
-               !st->tet_kf.p && !st->hex_kf.p && kind_ok && max_b <= kBatch;
+               !st->tet_kf.p && !st->hex_kf.p && kind_ok && max_b <= kBatch && offs_ok;
+    if (st->lean && sizeof(S) == 4) {
+      if (nts)
+        k_scale_conn<<<nblk(nts * 4), kBlk, 0, s>>>(st->tet_rec.p, nts / kBatch, RecBytes<S>(4), kBatch * 4, 1);
+      if (nhs)
+        k_scale_conn<<<nblk(nhs * 8), kBlk, 0, s>>>(st->hex_rec.p, nhs / kBatch, RecBytes<S>(8), kBatch * 8, 0);
+    }
   }
   if (nts)
     k_pack_slots<S><<<nblk(nts), kBlk, 0, s>>>(st->tet_slot_elem.p, nts, G_dev, 1.0,

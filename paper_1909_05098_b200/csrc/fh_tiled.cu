@@ -683,19 +683,26 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         g00 = G[i]; g01 = G[kBatch + i]; g02 = G[2 * kBatch + i];
         g11 = G[3 * kBatch + i]; g12 = G[4 * kBatch + i]; g22 = G[5 * kBatch + i];
       }
+      // Node references are used as BYTE offsets into sT and the accumulator
+      // rows.  The fp32 LEAN 1 records store them pre-multiplied by 4
+      // (k_scale_conn; no shift per corner), the others hold plain indices.
+      constexpr bool SCALED = LEAN == 1 && sizeof(S) == 4;
+      constexpr int SH = SCALED ? 0 : (sizeof(S) == 4 ? 2 : 3);
+      const unsigned char *sTb = reinterpret_cast<const unsigned char *>(sT);
+      unsigned char *accb = reinterpret_cast<unsigned char *>(acc);
+      const uint32_t nfreeb = (uint32_t)nfree * (uint32_t)sizeof(S);
       if constexpr (KINDS == 1) {
         const uint2 w = reinterpret_cast<const uint2 *>(stage)[i];
         const uint32_t raw[4] = {w.x & 0xffffu, w.x >> 16, w.y & 0xffffu, w.y >> 16};
-        uint16_t nd[4];
-        int rofs[4];
+        uint32_t nd[4], rofs[4];
 #pragma unroll
         for (int a = 0; a < 4; ++a) {  // LEAN tets always carry row-tagged connectivity (host condition)
-          nd[a] = (uint16_t)(raw[a] & 0x3fffu);
-          rofs[a] = (int)(raw[a] >> 14) * nfree;
+          nd[a] = (raw[a] & 0x3fffu) << SH;
+          rofs[a] = (raw[a] >> 14) * nfreeb;
         }
         S T[4];
 #pragma unroll
-        for (int b2 = 0; b2 < 4; ++b2) T[b2] = sT[nd[b2]];
+        for (int b2 = 0; b2 < 4; ++b2) T[b2] = *reinterpret_cast<const S *>(sTb + nd[b2]);
         // tet_loads with reg == 0 and kf == 1
         const S kb = kbar_lin<S, 4>(k0, T, kclamp, S(1));
         const S d1 = T[1] - T[0], d2 = T[2] - T[0], d3 = T[3] - T[0];
@@ -711,14 +718,14 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         // the first two phases are unrolled (1.3 phases per batch on cfg3)
         int loc[4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) loc[a] = nd[a] < nfree ? (int)nd[a] + rofs[a] : -1;
+        for (int a = 0; a < 4; ++a) loc[a] = nd[a] < nfreeb ? (int)(nd[a] + rofs[a]) : -1;
         auto rmw = [&]() {
           S old[4];
 #pragma unroll
-          for (int a = 0; a < 4; ++a) old[a] = loc[a] >= 0 ? acc[loc[a]] : S(0);
+          for (int a = 0; a < 4; ++a) old[a] = loc[a] >= 0 ? *reinterpret_cast<S *>(accb + loc[a]) : S(0);
 #pragma unroll
           for (int a = 0; a < 4; ++a)
-            if (loc[a] >= 0) acc[loc[a]] = old[a] - c[a];
+            if (loc[a] >= 0) *reinterpret_cast<S *>(accb + loc[a]) = old[a] - c[a];
         };
         (void)valid;
         if (ph == 0) rmw();
@@ -734,12 +741,13 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         }
       } else {
         const uint4 w = reinterpret_cast<const uint4 *>(stage)[i];
-        uint16_t nd[kSPT][8];
-        nd[0][0] = w.x & 0xffff; nd[0][1] = w.x >> 16; nd[0][2] = w.y & 0xffff; nd[0][3] = w.y >> 16;
-        nd[0][4] = w.z & 0xffff; nd[0][5] = w.z >> 16; nd[0][6] = w.w & 0xffff; nd[0][7] = w.w >> 16;
+        uint32_t nd[kSPT][8];
+        nd[0][0] = (w.x & 0xffff) << SH; nd[0][1] = (w.x >> 16) << SH; nd[0][2] = (w.y & 0xffff) << SH;
+        nd[0][3] = (w.y >> 16) << SH; nd[0][4] = (w.z & 0xffff) << SH; nd[0][5] = (w.z >> 16) << SH;
+        nd[0][6] = (w.w & 0xffff) << SH; nd[0][7] = (w.w >> 16) << SH;
         S T[8];
 #pragma unroll
-        for (int b2 = 0; b2 < 8; ++b2) T[b2] = sT[nd[0][b2]];
+        for (int b2 = 0; b2 < 8; ++b2) T[b2] = *reinterpret_cast<const S *>(sTb + nd[0][b2]);
         // hex_loads with reg == 0 and kf == 1
         const S kb = kbar_lin<S, 8>(k0, T, kclamp, S(1));
         const S gx = ((T[1] - T[0]) + (T[2] - T[3])) + ((T[5] - T[4]) + (T[6] - T[7]));
@@ -755,13 +763,14 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         // two-row corner phases (accumulate<kCornerPhase2>): corners a and a+4
         // go to different rows, so both read-modify-writes issue together
         (void)valid;
-        S *acc1 = acc + nfree;
+        unsigned char *acc1b = accb + nfreeb;
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
-          const int l0 = nd[0][a] < nfree ? (int)nd[0][a] : -1, l1 = nd[0][a + 4] < nfree ? (int)nd[0][a + 4] : -1;
-          const S o0 = l0 >= 0 ? acc[l0] : S(0), o1 = l1 >= 0 ? acc1[l1] : S(0);
-          if (l0 >= 0) acc[l0] = o0 - c[0][a];
-          if (l1 >= 0) acc1[l1] = o1 - c[0][a + 4];
+          const bool u0 = nd[0][a] < nfreeb, u1 = nd[0][a + 4] < nfreeb;
+          S *p0 = reinterpret_cast<S *>(accb + nd[0][a]), *p1 = reinterpret_cast<S *>(acc1b + nd[0][a + 4]);
+          const S o0 = u0 ? *p0 : S(0), o1 = u1 ? *p1 : S(0);
+          if (u0) *p0 = o0 - c[0][a];
+          if (u1) *p1 = o1 - c[0][a + 4];
           __syncthreads();
           if (a == 0) refill();
         }

@@ -269,6 +269,12 @@ int fh_get_node_order(fh_engine *e, int64_t *new_to_old, int64_t n);
 /* multi-GPU: NCCL bootstrap.  Rank 0 creates the id (128 bytes), the
  * caller broadcasts it (torch.distributed), every rank attaches. */
 int fh_nccl_unique_id(char *id128);
+/* NCCL is loaded with dlopen the first time it is needed: a libnccl.so.2 the
+ * process already holds, else `path` (if set here), else the sonames
+ * libnccl.so.2 / libnccl.so.  A host that later loads a framework bundling its
+ * own NCCL (PyTorch) should name that file here, so that the one NCCL in the
+ * process is the version the framework was built against. */
+int fh_nccl_library(const char *path);
 /* world == 1 builds a one-rank communicator (the fail-flag all-reduce then
  * goes through NCCL): a single-GPU check of the NCCL loading and init path */
 int fh_attach_nccl(fh_engine *e, const char *id128, int32_t rank, int32_t world);

@@ -103,7 +103,7 @@ EXPORTS = [
     "fh_element_mean_nodal", "fh_scatter_net_loads", "fh_nodal_update", "fh_create", "fh_destroy",
     "fh_set_temperature", "fh_get_temperature", "fh_get_inflow", "fh_keep_inflow", "fh_reset_properties", "fh_step",
     "fh_step_timed", "fh_step_timed_flush", "fh_step_host", "fh_step_host_async", "fh_host_wait", "fh_set_q_static", "fh_set_sources", "fh_set_probes", "fh_get_probes", "fh_critical_dt", "fh_scatter_loads",
-    "fh_get_precompute", "fh_get_layout", "fh_stream", "fh_get_node_order", "fh_nccl_unique_id",
+    "fh_get_precompute", "fh_get_layout", "fh_stream", "fh_get_node_order", "fh_nccl_unique_id", "fh_nccl_library",
     "fh_attach_nccl", "fh_attach_transport", "fh_halo_info", "fh_halo_lists", "fh_halo_export", "fh_halo_import", "fh_get_owned",
     "fh_plan_create", "fh_plan_info", "fh_plan_arrays", "fh_plan_destroy", "fh_mesh_parse", "fh_mesh_text_info",
     "fh_mesh_text_arrays", "fh_mesh_text_set", "fh_mesh_text_destroy", "fh_format_f64", "fh_format_i64",
@@ -154,6 +154,21 @@ def lib():
     L.fh_scatter_net_loads.argtypes = [i64p, i64p, f64p, i64p, C.c_int64, f64p, f64p, C.c_int64, C.c_int64, f64p]
     L.fh_nodal_update.argtypes = [f64p, f64p, f64p, f64p, f64p, f64p, f64p, C.c_int64, C.c_double]
     L.fh_nccl_unique_id.argtypes = [C.c_char_p]
+    L.fh_nccl_library.argtypes = [C.c_char_p]
+    # one NCCL per process: prefer the copy PyTorch bundles (found without
+    # importing torch), so that the library's dlopen and a later `import torch`
+    # agree on the version behind the libnccl.so.2 soname
+    try:
+        import importlib.util
+
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for d in (spec.submodule_search_locations if spec else []):
+            cand = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                L.fh_nccl_library(cand.encode())
+                break
+    except Exception:  # pragma: no cover - best effort, the sonames remain
+        pass
     L.fh_attach_nccl.argtypes = [C.c_void_p, C.c_char_p, C.c_int32, C.c_int32]
     L.fh_attach_transport.argtypes = [C.c_void_p, C.POINTER(FhTransport)]
     i32o = C.POINTER(C.c_int32)

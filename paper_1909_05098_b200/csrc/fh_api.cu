@@ -11,6 +11,7 @@
 #include "fh_dist.h"
 #include "fh_tiled.cuh"
 #include "fh_resident.h"
+#include <limits>
 #include "fh_atomic.h"
 
 using namespace fh;
@@ -971,6 +972,17 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   g.robin_hAT = st->robin_hAT.p;
   g.mats = mats_of<S>(e);
   g.lin = normalise_curves(g.mats);
+  g.lin_lo = -std::numeric_limits<S>::infinity();
+  g.lin_hi = std::numeric_limits<S>::infinity();
+  if (g.lin) {
+    const Mat<S> &m0 = g.mats.m[0];
+    const Curve<S> *cs[4] = {&m0.rho, &m0.c, &m0.k, m0.td_perf ? &m0.wb : nullptr};
+    for (const Curve<S> *c : cs)
+      if (c && c->n == 2 && c->slope[0] != S(0)) {
+        g.lin_lo = std::max(g.lin_lo, c->x[0]);
+        g.lin_hi = std::min(g.lin_hi, c->x[1]);
+      }
+  }
   g.tet_rows = P.tet_rows;
   g.n_src = 0;  // set per step from the active sources
   g.n_gauss = 0;
@@ -991,7 +1003,8 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   if (o.tile_stages > 0) g.n_stages = std::min(kMaxStages, o.tile_stages);
   // +1: the dummy node the padding slots point at (partition step 5)
   // staged per node: T, plus k(T) only for laws with more than two knots (fh_tiled.cu, Staged)
-  g.smem_T = (int)al((e->td && !g.lin ? 2 : 1) * sizeof(S) * ((size_t)std::max(1, P.max_local_nodes) + 1));
+  // (+4: the owned range is bulk-copied from the 16-byte boundary below its first node)
+  g.smem_T = (int)al((e->td && !g.lin ? 2 : 1) * sizeof(S) * ((size_t)std::max(1, P.max_local_nodes) + 1 + 4));
   // +1: the trash slot of the corner-phase accumulation
   const int rows = std::max(st->mode == kModeCornerPhase2 ? 2 : 1,
                             P.tet_rows);
@@ -2396,6 +2409,12 @@ int fh_nodal_update(double *temps, const double *inflow, const double *capacity,
   qr.upload(extra_q, n);
   op_update(T.p, F.p, C.p, kb.p, qb.p, qm.p, qr.p, n, dt, 0);
   FH_CUDA(cudaMemcpy(temps, T.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  FH_API_END
+}
+
+int fh_nccl_library(const char *path) {
+  FH_API_BEGIN
+  nccl_set_library(path);
   FH_API_END
 }
 

@@ -25,12 +25,18 @@ struct NcclApi {
   const char *(*GetErrorString)(int) = nullptr;
 };
 NcclApi g_nccl;
+std::string g_nccl_path;  // preferred library file (nccl_set_library), tried before the sonames
 
 void load_nccl() {
   if (g_nccl.h) return;
-  const char *names[] = {"libnccl.so.2", "libnccl.so"};
-  for (const char *n : names)
-    if ((g_nccl.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+  // a libnccl.so.2 the process already holds (e.g. the one bundled with
+  // PyTorch) is reused by soname; otherwise the preferred file comes first, so
+  // that a framework imported LATER finds the version it was built against
+  // under that soname instead of an older system copy
+  const char *names[] = {g_nccl_path.empty() ? nullptr : g_nccl_path.c_str(), "libnccl.so.2", "libnccl.so"};
+  if ((g_nccl.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD)) == nullptr)
+    for (const char *n : names)
+      if (n && (g_nccl.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
   if (!g_nccl.h) fail(FH_ERR_DEVICE, std::string("cannot load NCCL: ") + dlerror());
   auto sym = [](const char *s) {
     void *p = dlsym(g_nccl.h, s);
@@ -55,6 +61,8 @@ void nccl_check(int rc, const char *what) {
 // ncclDataType_t / ncclRedOp_t values of nccl.h
 constexpr int kNcclUint64 = 5, kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclMin = 3;
 }  // namespace
+
+void nccl_set_library(const char *path) { g_nccl_path = path ? path : ""; }
 
 void nccl_unique_id(NcclUniqueId *id) {
   load_nccl();

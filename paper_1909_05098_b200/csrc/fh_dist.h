@@ -8,6 +8,8 @@ struct NcclUniqueId {
   char internal[128];  // layout of ncclUniqueId (nccl.h, NCCL_UNIQUE_ID_BYTES)
 };
 
+// file to dlopen for NCCL before the default sonames (empty / null: sonames only); no effect once NCCL is loaded
+void nccl_set_library(const char *path);
 void nccl_unique_id(NcclUniqueId *id);
 void *nccl_comm_init(const NcclUniqueId &id, int rank, int world);
 void nccl_comm_destroy(void *comm);

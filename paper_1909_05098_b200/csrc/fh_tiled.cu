@@ -204,12 +204,21 @@ __device__ __forceinline__ double fast_exp(double x) { return exp(x); }
 
 // F - kb T + qb + qm + q_ext with C, kb from the material laws (TD) or the
 // frozen arrays (TI); returns the rate, writes the capacity
-template <typename S, bool TD, bool LIN>
+// INSIDE: x lies strictly between the knots of every two-knot law of the
+// material (the tile's `kclamp` flag is clear), so the clamps of ip<true> are
+// skipped -- the remaining FMA is ip<true>'s own, bit for bit
+template <bool LIN, bool INSIDE, typename S>
+__device__ __forceinline__ S ipn(const Curve<S> &c, S x) {
+  if (LIN && INSIDE) return c.slope[0] * (x - c.x[0]) + c.y[0];
+  return ip<LIN>(c, x);
+}
+
+template <typename S, bool TD, bool LIN, bool INSIDE = false>
 __device__ __forceinline__ S node_rate(const Mat<S> &m, S x, S F, S v, S q, S cfrozen, S kbfrozen, S &cap) {
   S kb;
   if (TD) {
-    cap = ip<LIN>(m.rho, x) * ip<LIN>(m.c, x) * v;
-    kb = m.td_perf ? ip<LIN>(m.wb, x) * m.cb * v : m.wbcb * v;
+    cap = ipn<LIN, INSIDE>(m.rho, x) * ipn<LIN, INSIDE>(m.c, x) * v;
+    kb = m.td_perf ? ipn<LIN, INSIDE>(m.wb, x) * m.cb * v : m.wbcb * v;
   } else {
     cap = cfrozen;
     kb = m.td_perf ? kbfrozen : m.wbcb * v;
@@ -506,12 +515,12 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr bool KST = TD && !LIN;  // stage (T, k(T)) pairs; otherwise T alone (see Staged)
   using ST = Staged<S, KST>;
-  ST *sT = reinterpret_cast<ST *>(smem);
   S *acc = reinterpret_cast<S *>(smem + g.smem_T);
   unsigned char *ring = smem + g.smem_T + g.smem_acc;
   const int kStages = g.n_stages;
   __shared__ __align__(8) uint64_t bars[kMaxStages];
   __shared__ __align__(8) uint64_t hbar;  // halo id list copy
+  __shared__ __align__(8) uint64_t tbar;  // owned temperature range copy (T-only staging)
   __shared__ int s_bad;
   // phases per batch of the tile (colour modes), read once instead of per batch
   constexpr int kNphCache = kTileThreads;  // one phase-count byte per batch, filled by one thread each
@@ -524,6 +533,13 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   const int n0 = g.part_node_start[p];
   const int nn = g.part_node_start[p + 1] - n0;
   const int nfree = g.part_n_free[p];
+  // T-only staging: the owned range Tin[n0, n0 + nn) is one bulk copy from the
+  // 16-byte boundary below n0, so the tile's node 0 sits `lead` elements into
+  // the staging region (the elements before it are never referenced)
+  constexpr int kVec = 16 / (int)sizeof(S);
+  const int lead = KST ? 0 : (n0 & (kVec - 1));
+  ST *sT = reinterpret_cast<ST *>(smem) + lead;
+  const int n_bulk = KST ? 0 : ((lead + nn) & ~(kVec - 1));  // elements the bulk copy brings (from n0 - lead)
   // tile tables read once (the batch loop would otherwise re-load them every iteration)
   const int t_cnt = __ldg(g.part_tet_count + p), h_cnt = __ldg(g.part_hex_count + p);
   const int t_start = __ldg(g.part_tet_start + p), h_start = __ldg(g.part_hex_start + p);
@@ -551,6 +567,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
 #pragma unroll
     for (int q = 0; q < kStages; ++q) mbar_init(&bars[q], 1);
     mbar_init(&hbar, 1);
+    mbar_init(&tbar, 1);
     fence_barrier_init();
   }
   __syncthreads();  // the mbarriers are initialised before anyone waits on them
@@ -558,6 +575,10 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
     const uint32_t hbytes = (uint32_t)((((h0 + nh + 3) & ~3) - hs) * 4);
     mbar_expect_tx(&hbar, hbytes);
     if (hbytes) bulk_g2s(s_ids, g.halo_nodes + hs, hbytes, &hbar);
+    if constexpr (!KST) {
+      mbar_expect_tx(&tbar, (uint32_t)(n_bulk * sizeof(S)));
+      if (n_bulk) bulk_g2s(smem, g.Tin + (n0 - lead), (uint32_t)(n_bulk * sizeof(S)), &tbar);
+    }
     for (int j = 0; j < kStages && j < nb; ++j) {
       if constexpr (LEAN)
         lean_issue<S, KINDS == 1 ? 4 : 8>(g, KINDS == 1 ? t_start : h_start, j, ring + j * g.stage_bytes, &bars[j]);
@@ -576,31 +597,41 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
   // so the unrolled rounds stay branch-free.  Two-knot laws stage T alone and
   // note whether any staged temperature lies outside material 0's conductivity
   // knots (kout -> kclamp); laws with more knots stage k(T) of material 0 too.
+  // (kout is set by any staged temperature that is not strictly inside
+  // (g.lin_lo, g.lin_hi), the intersection of the knot ranges of material 0's
+  // sloped laws -- k, rho, c, w_b -- so the flag also lets the node update of
+  // LEAN tiles skip its clamps; NaN counts as outside)
   const Curve<S> &k0 = g.mats.m[0].k;
-  const S kx0 = k0.x[0], kx1 = k0.x[1];
-  const bool ksloped = TD && LIN && k0.slope[0] != S(0);
+  const S kx0 = g.lin_lo, kx1 = g.lin_hi;
+  const bool ksloped = TD && LIN;
   bool kout = false;
   auto staged = [&](S x) -> ST {
     if constexpr (KST) {
       return TK<S>{x, interp(k0, x)};
     } else {
-      if (TD && LIN) kout |= (x < kx0) | (x > kx1);
+      if (TD && LIN) kout |= !((x > kx0) & (x < kx1));
       return x;
     }
   };
   // loads in flight per thread while staging (tet-only tiles: 4, measured
   // 1% faster on cfg3; hex tiles: 8)
   constexpr int U = KINDS == 1 ? FH_STAGE_UNROLL_TET : FH_STAGE_UNROLL;
-  for (int base = tid; base < nn; base += U * kTileThreads) {
-    S x[U];
+  if constexpr (KST) {
+    for (int base = tid; base < nn; base += U * kTileThreads) {
+      S x[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) x[u] = __ldg(g.Tin + n0 + min(base + u * kTileThreads, nn - 1));
+      for (int u = 0; u < U; ++u) x[u] = __ldg(g.Tin + n0 + min(base + u * kTileThreads, nn - 1));
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = base + u * kTileThreads;
-      const ST v = staged(x[u]);
-      if (i < nn) sT[i] = v;
+      for (int u = 0; u < U; ++u) {
+        const int i = base + u * kTileThreads;
+        const ST v = staged(x[u]);
+        if (i < nn) sT[i] = v;
+      }
     }
+  } else {
+    // the (at most kVec - 1) owned nodes past the bulk copy's last 16 bytes
+    const int i = n_bulk - lead + tid;
+    if (i < nn) sT[i] = staged(__ldg(g.Tin + n0 + i));
   }
   mbar_wait(&hbar, 0);
   for (int base = tid; base < nh; base += U * kTileThreads) {
@@ -618,6 +649,23 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       const int i = base + u * kTileThreads;
       const ST v = staged(x[u]);
       if (i < nh) sT[nn + i] = v;
+    }
+  }
+  if constexpr (!KST) {
+    mbar_wait(&tbar, 0);
+    if (ksloped) {  // knots check of the bulk-copied owned nodes (16 bytes per load)
+      for (int v = tid; v < n_bulk / kVec; v += kTileThreads) {
+        S x[kVec];
+        if constexpr (sizeof(S) == 4) {
+          const float4 q = reinterpret_cast<const float4 *>(smem)[v];
+          x[0] = q.x; x[1] = q.y; x[2] = q.z; x[3] = q.w;
+        } else {
+          const double2 q = reinterpret_cast<const double2 *>(smem)[v];
+          x[0] = q.x; x[1] = q.y;
+        }
+#pragma unroll
+        for (int c = 0; c < kVec; ++c) kout |= !((x[c] > kx0) & (x[c] < kx1)) & (v * kVec + c >= lead);
+      }
     }
   }
   if (tid == 0) sT[nn + nh] = ST{};  // the padding slots' dummy node (partition step 5): T = 0
@@ -885,8 +933,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
                                                           : (g.node_region ? (FH_PART_MAT ? (int)g.part_mat[p] : -1) : 0);
   // nodes per thread per round: their global loads are issued together
   constexpr int UN = KINDS == 1 ? FH_NODE_UNROLL_TET : FH_NODE_UNROLL;
-  auto node_loop = [&](auto kind_tag) {
+  auto node_loop = [&](auto kind_tag, auto inside_tag) {
     constexpr int KIND = decltype(kind_tag)::value;
+    constexpr bool INSIDE = decltype(inside_tag)::value;
     for (int base = tid; base < nfree; base += UN * kTileThreads) {
       S v[UN], q[UN], cf[UN], kf[UN], px[UN], py[UN], pz[UN];
 #pragma unroll
@@ -925,7 +974,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
         S rate;
         S cap;
         if (KIND != 0)  // single material: curve parameters are uniform operands
-          rate = node_rate<S, TD, LIN>(g.mats.m[tm], x, Fsum, v[u], q[u], cf[u], kf[u], cap);
+          rate = node_rate<S, TD, LIN, INSIDE>(g.mats.m[tm], x, Fsum, v[u], q[u], cf[u], kf[u], cap);
         else if (!g.node_region)
           rate = node_rate<S, TD, LIN>(g.mats.m[0], x, Fsum, v[u], q[u], cf[u], kf[u], cap);
         else
@@ -957,14 +1006,24 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
     }
   };
   const bool simple = tm >= 0 && rstart >= nfree;
-  if (simple && g.n_src == 0)
-    node_loop(std::integral_constant<int, 1>{});
-  else if (simple && g.n_src == 1 && g.n_gauss == 1)
-    node_loop(std::integral_constant<int, 2>{});
-  else if (simple && g.n_src == 1)
-    node_loop(std::integral_constant<int, 3>{});
-  else
-    node_loop(std::integral_constant<int, 0>{});
+  // LEAN tiles (material 0 throughout) whose staged temperatures all lie inside the laws' knots skip the clamps
+  const bool inside = LEAN != 0 && TD && LIN && tm == 0 && !kclamp;
+  auto node_kind = [&](auto inside_tag) {
+    if (simple && g.n_src == 0)
+      node_loop(std::integral_constant<int, 1>{}, inside_tag);
+    else if (simple && g.n_src == 1 && g.n_gauss == 1)
+      node_loop(std::integral_constant<int, 2>{}, inside_tag);
+    else if (simple && g.n_src == 1)
+      node_loop(std::integral_constant<int, 3>{}, inside_tag);
+    else
+      node_loop(std::integral_constant<int, 0>{}, std::false_type{});
+  };
+  if constexpr (LEAN != 0) {
+    if (inside) node_kind(std::true_type{});
+    else node_kind(std::false_type{});
+  } else {
+    node_kind(std::false_type{});
+  }
   if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) s_bad = 1;
   __syncthreads();
   if (tid == 0 && s_bad) atomicMin(&g.flag->step, g.step_no);

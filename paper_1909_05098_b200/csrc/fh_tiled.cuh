@@ -57,6 +57,7 @@ struct TiledArgs {
   const S *robin_hA, *robin_hAT;
   MatSet<S> mats;   // one-knot curves normalised to two knots (see normalise_curves)
   int lin;          // every curve has <= 2 knots: branch-free interpolation kernels
+  S lin_lo, lin_hi; // lin: intersection of the knot ranges of material 0's sloped laws (open interval)
   int tet_rows;     // tet accumulator rows (1 or 4; tet-only meshes), see Partition::tet_rows
   int n_gauss;      // active sources, Gaussians first: src[0, n_gauss) Gaussian, [n_gauss, n_src) RF
   int n_src;

@@ -136,3 +136,47 @@ def test_cfg5_family_mixed_voxel_regions(assembly, prec, tol):
         assert np.array_equal(res.state.temperatures, T_ref)
     else:
         assert rel(res.state.temperatures, T_ref) <= tol
+
+
+def clamped_material():
+    """Two-knot laws whose knots lie INSIDE the temperatures of the run: part
+    of the field is interpolated, part is clamped (np.interp semantics)."""
+    from paper_1909_05098_b200.material import linear_law, make_constant
+
+    return fh.TissueMaterial(
+        density=make_constant(1060.0), specific_heat=linear_law(3600.0, -0.0005, 37.0, t_lo=36.6, t_hi=37.8),
+        conductivity=linear_law(0.5, 0.02, 37.0, t_lo=36.8, t_hi=37.6), perfusion_rate=0.525,
+        blood_specific_heat=3640.0, arterial_temperature=37.0, metabolic_rate=420.0,
+        perfusion_curve=linear_law(0.525, configs.PERFUSION_SLOPE, 37.0, t_lo=36.9, t_hi=37.4))
+
+
+@pytest.mark.parametrize("kind", ["hex", "tet", "mixed"])
+@pytest.mark.parametrize("prec,tol", [(64, 1e-10), (32, 1e-4)])
+def test_tiled_two_knot_laws_clamp_outside_their_knots(kind, prec, tol):
+    """The fused step stages T alone for two-knot laws and takes k(mean T) per
+    slot; tiles holding a temperature outside the conductivity knots must fall
+    back to per-corner clamped interpolation (fh_tiled.cu kbar_lin).  A field
+    that straddles both knots, in tiles of all three kinds, against the oracle;
+    the LEAN loops and the general kernel agree bit for bit."""
+    if kind == "mixed":
+        mesh = configs.cfg5(scale=16).mesh
+    else:
+        mesh = fh.jittered_cube_mesh(kind, 10, 0.1, 0.15, seed=5)
+    mat = clamped_material()
+    rng = np.random.default_rng(8)
+    # a smooth ramp from 36.2 to 38.4 C across x plus noise: some tiles entirely
+    # between the knots, some entirely outside, some straddling them
+    x = mesh.nodes[:, 0]
+    T0 = 36.2 + 2.2 * (x - x.min()) / (x.max() - x.min()) + rng.uniform(-0.05, 0.05, mesh.n_nodes)
+    fields = []
+    for lean in (0, 1):
+        eng = fh.ExplicitEngine(mesh, mat, assembly="tiled", precision=prec, part_nodes=200,
+                                tuning={"lean_kernels": lean})
+        dt = 0.8 * eng.critical_dt(T0)
+        fields.append(eng.run(T0, steps=40, dt=dt).state.temperatures)
+    assert np.array_equal(fields[0], fields[1])
+    ora = orc.OracleModel(mesh, mat, td_mode=True)
+    T_ref, _ = ora.run(T0, 40, dt)
+    assert np.abs(T_ref - T0).max() > 1e-3
+    assert float(np.abs(fields[0] - T_ref).max() / np.abs(T_ref - T0).max()) <= tol
+    assert rel(fields[0], T_ref) <= tol

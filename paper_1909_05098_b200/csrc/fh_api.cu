@@ -196,7 +196,8 @@ struct TiledState {
   int n_boundary = 0;  // multi-GPU: leading entries of part_list that touch the halo
   // tiles with tets at the head of the boundary / interior ranges (mixed meshes)
   int n_mixed_b = 0, n_mixed_i = 0;
-  int n_lean_i = 0;  // one GPU, regions: material-0 hex-only tiles at the end of the list (LEAN 2 launch)
+  int n_lean_i = 0;  // one GPU, regions / mixed mesh: material-0 hex-only tiles at the end of the list (LEAN 2 launch)
+  int n_lean_mixed_i = 0;  // ... and the material-0 tiles holding tets, at the end of the mixed range (LEAN 3 launch)
   int mode = 0;
   bool lean = false;  // LEAN loops and their paired-G records
 };
@@ -701,25 +702,36 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
     st->n_mixed_b = (int)(mid_b - plist.begin());
     st->n_mixed_i = (int)(mid_i - (plist.begin() + st->n_boundary));
   }
-  // one GPU with material regions: the hex-only tiles whose slots all lie in
-  // region 0 go last and run the LEAN 2 loop (fh_tiled.cu), the others keep
-  // the general kernel
-  if (e->X.world == 1 && o.n_materials > 1 && o.element_region && e->td && o.lean_kernels == 0 &&
+  // one GPU, a mesh with material regions or with both element kinds: the
+  // hex-only tiles whose slots all lie in region 0 go last and run the LEAN 2
+  // loop (fh_tiled.cu); the region-0 tiles that hold tets go to the end of the
+  // mixed range and run the LEAN 3 loop; the others keep the general kernel
+  const bool has_regions = o.n_materials > 1 && o.element_region;
+  if (e->X.world == 1 && (has_regions || split) && e->td && o.lean_kernels == 0 && o.tile_mode == 0 &&
       P.corner_unique && sizeof(S) == 4 && !(e->kfactor.p && !e->td)) {
     MatSet<S> mt = mats_of<S>(e);
     bool ok = normalise_curves(mt) != 0;
     for (int q = 0; q < P.n_parts && ok; ++q)
       ok = (P.part_hex_count[q] + kBatch - 1) / kBatch + (P.part_tet_count[q] + kBatch - 1) / kBatch <= kBatch;
     auto region0 = [&](int32_t p) {
-      if (P.part_tet_count[p] > 0) return false;
+      if (!has_regions) return true;
       for (int32_t q = P.part_hex_start[p]; q < P.part_hex_start[p] + P.part_hex_count[p]; ++q)
         if (P.hex_slot_elem[q] >= 0 && o.element_region[P.hex_slot_elem[q]] != 0) return false;
+      for (int32_t q = P.part_tet_start[p]; q < P.part_tet_start[p] + P.part_tet_count[p]; ++q)
+        if (P.tet_slot_elem[q] >= 0 && o.element_region[P.tet_slot_elem[q]] != 0) return false;
       return true;
     };
     if (ok) {
       auto first = plist.begin() + st->n_boundary + st->n_mixed_i;
-      auto mid = std::stable_partition(first, plist.end(), [&](int32_t p) { return !region0(p); });
+      auto mid = std::stable_partition(first, plist.end(),
+                                       [&](int32_t p) { return !(P.part_tet_count[p] == 0 && region0(p)); });
       st->n_lean_i = (int)(plist.end() - mid);
+      // tets in colour phases with one accumulator row and plain 14-bit node references
+      if (P.colored_ok && P.tet_rows == 1 && P.max_local_nodes + 1 < (1 << 14)) {
+        auto mfirst = plist.begin() + st->n_boundary;
+        auto mmid = std::stable_partition(mfirst, mfirst + st->n_mixed_i, [&](int32_t p) { return !region0(p); });
+        st->n_lean_mixed_i = (int)((mfirst + st->n_mixed_i) - mmid);
+      }
     }
   }
   st->part_list.upload(plist, s);
@@ -1213,7 +1225,15 @@ void tiled_run(fh_engine *e, int64_t nsteps, double dt) {
       }
       FH_CUDA(cudaEventRecord(e->ev_fork, e->stream));
       FH_CUDA(cudaStreamWaitEvent(e->kind_stream, e->ev_fork, 0));
-      tiled_step(g, n_mixed, e->td, st.mode, st.smem, e->kind_stream);
+      // the material-0 mixed tiles (end of the mixed range) run the LEAN 3 loop
+      const int n_lm = (e->X.world == 1 && begin == st.n_boundary) ? std::min(st.n_lean_mixed_i, n_mixed) : 0;
+      tiled_step(g, n_mixed - n_lm, e->td, st.mode, st.smem, e->kind_stream);
+      if (n_lm > 0) {
+        TiledArgs<S> gm = g;
+        gm.part_begin = begin + n_mixed - n_lm;
+        gm.lean = 3;
+        tiled_step(gm, n_lm, e->td, st.mode, st.smem, e->kind_stream);
+      }
       FH_CUDA(cudaEventRecord(e->ev_join, e->kind_stream));
       TiledArgs<S> gh = g;
       gh.tet_rec = nullptr;
@@ -2236,6 +2256,7 @@ int fh_get_layout(fh_engine *e, fh_layout *out) {
     auto launches = [&](const auto &st) {  // one per tile kind present in each launch range
       const int ni = st.n_parts_local - st.n_boundary;
       return (st.n_mixed_i > 0 && st.n_mixed_i < ni ? 2 : 1) + (st.n_lean_i > 0 && st.n_lean_i < ni - st.n_mixed_i ? 1 : 0) +
+             (st.n_mixed_i < ni && st.n_lean_mixed_i > 0 && st.n_lean_mixed_i < st.n_mixed_i ? 1 : 0) +
              (st.n_boundary ? (st.n_mixed_b > 0 && st.n_mixed_b < st.n_boundary ? 2 : 1) : 0);
     };
     out->kernels_per_step = e->precision == 32 ? launches(*e->tf) : launches(*e->tdd);

@@ -304,6 +304,14 @@ __device__ __forceinline__ void lean_issue(const TiledArgs<S> &g, int s_start, i
   if (N == 4) bulk_g2s(stage + RecBytes<S>(N), g.tet_phase + s_start + j * kBatch, kBatch, bar);
 }
 
+// LEAN 3 (mixed tiles): batch j of the tile is a tet batch while j < nbt, then a hex batch
+template <typename S>
+__device__ __forceinline__ void lean_issue_mixed(const TiledArgs<S> &g, int t_start, int h_start, int nbt, int j,
+                                                 unsigned char *stage, uint64_t *bar) {
+  if (j < nbt) lean_issue<S, 4>(g, t_start, j, stage, bar);
+  else lean_issue<S, 8>(g, h_start, j - nbt, stage, bar);
+}
+
 // element loads of staged slot i of the batch ------------------------------------
 template <typename S, bool TD, bool LIN>
 __device__ __forceinline__ void hex_loads(const TiledArgs<S> &g, const unsigned char *stage,
@@ -506,8 +514,10 @@ __device__ __forceinline__ void accumulate_colored(S *acc, const uint16_t (&nd)[
 // per-slot kf / region / rank streams -- with every per-batch flag and stage
 // offset a compile-time constant (same arithmetic, same bits).  LEAN 1: the
 // whole launch (fp32 records with paired G rows); LEAN 2: the material-0
-// hex-only tiles of a mesh with regions (component-row G, like the general
-// kernel's tiles of the same launch family).
+// hex-only tiles of a mixed mesh or a mesh with regions (component-row G, like
+// the general kernel's tiles of the same launch family); LEAN 3: the
+// material-0 tiles of such a mesh that hold tets and hexes (one-row colour
+// phases for the tet batches, then the hex batches).
 template <typename S, bool TD, int MODE, int KINDS, bool LIN, int LEAN = 0>
 __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? kMinBlocksTet : kMinBlocksF32)
                                                                 : (KINDS == 1 ? kMinBlocksTetF64 : 2))
@@ -580,7 +590,9 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       if (n_bulk) bulk_g2s(smem, g.Tin + (n0 - lead), (uint32_t)(n_bulk * sizeof(S)), &tbar);
     }
     for (int j = 0; j < kStages && j < nb; ++j) {
-      if constexpr (LEAN)
+      if constexpr (LEAN && KINDS == 2)
+        lean_issue_mixed<S>(g, t_start, h_start, nbt, j, ring + j * g.stage_bytes, &bars[j]);
+      else if constexpr (LEAN)
         lean_issue<S, KINDS == 1 ? 4 : 8>(g, KINDS == 1 ? t_start : h_start, j, ring + j * g.stage_bytes, &bars[j]);
       else
         issue_batch(g, p, j, nbt, ring + j * g.stage_bytes, &bars[j], preg < 0);
@@ -691,9 +703,8 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
     return jj < kNphCache ? (int)s_nph[jj] : (int)__ldg(bn + slot0 / kBatch);
   };
   if constexpr (LEAN) {
-    constexpr int N = KINDS == 1 ? 4 : 8;
     // stage layout without kf / region / rank blocks: conn16 | G | phase (tets)
-    constexpr int kG = kBatch * N * 2, kPhase = kG + 6 * kBatch * (int)sizeof(S);
+    constexpr int kGt = kBatch * 4 * 2, kGh = kBatch * 8 * 2, kPhase = kGt + 6 * kBatch * (int)sizeof(S);
     const int sbytes = g.stage_bytes;
     const uint32_t bar0 = smem_u32(&bars[0]);
     const int cnt = KINDS == 1 ? t_cnt : h_cnt;
@@ -716,9 +727,13 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       auto refill = [&]() {
         if (tid == 0 && j + kStages < nb) {
           fence_proxy_async();
-          lean_issue<S, N>(g, KINDS == 1 ? t_start : h_start, j + kStages, stage, &bars[st]);
+          if constexpr (KINDS == 2) lean_issue_mixed<S>(g, t_start, h_start, nbt, j + kStages, stage, &bars[st]);
+          else lean_issue<S, KINDS == 1 ? 4 : 8>(g, KINDS == 1 ? t_start : h_start, j + kStages, stage, &bars[st]);
         }
       };
+      // mixed tiles (LEAN 3): the tile's tet batches come first
+      const bool tet_batch = KINDS == 1 || (KINDS == 2 && j < nbt);
+      const int kG = tet_batch ? kGt : kGh;
       // fp32: paired G rows (k_pack_slots) (00,01) (02,11) (12,22), one 8-byte
       // load each; fp64: the 6 component rows
       S g00, g01, g02, g11, g12, g22;
@@ -739,7 +754,7 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       const unsigned char *sTb = reinterpret_cast<const unsigned char *>(sT);
       unsigned char *accb = reinterpret_cast<unsigned char *>(acc);
       const uint32_t nfreeb = (uint32_t)nfree * (uint32_t)sizeof(S);
-      if constexpr (KINDS == 1) {
+      if (KINDS != 0 && tet_batch) {
         const uint2 w = reinterpret_cast<const uint2 *>(stage)[i];
         const uint32_t raw[4] = {w.x & 0xffffu, w.x >> 16, w.y & 0xffffu, w.y >> 16};
         uint32_t nd[4], rofs[4];
@@ -1069,8 +1084,11 @@ void (*pick_step_kernel(const TiledArgs<S> &g, bool td, int mode_sel, size_t sme
   } else if (g.lean == 2 && kinds == 0) {
     kern = k_tiled_step<S, true, kCornerPhase2, 0, true, 2>;
     lean = 3;
+  } else if (g.lean == 3 && kinds == 2) {
+    kern = k_tiled_step<S, true, kCornerPhase2, 2, true, 3>;
+    lean = 4;
   }
-  static size_t configured[4][2][2][3][7] = {};
+  static size_t configured[5][2][2][3][7] = {};
   size_t &cfg = configured[lean][lin][td ? 1 : 0][kinds][mode];
   if (smem > cfg) {
     FH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -2009,7 +2009,15 @@ int fh_step_host_async(fh_engine *e, const double *T_in, double *T_out, int64_t 
   else
     tiled_set_T<double>(e, e->io_in[slot].p);
   FH_CUDA(cudaEventRecord(ev[1], e->stream));
-  run_steps(e, nsteps, dt);
+  {
+    // an asynchronous call cannot replay a runaway: several steps per call keep
+    // the resident kernel's grid barrier, which stops every CTA at the failing step
+    unsigned long long *ll[2] = {e->res.ll[0], e->res.ll[1]};
+    if (nsteps > 1) e->res.ll[0] = e->res.ll[1] = nullptr;
+    run_steps(e, nsteps, dt);
+    e->res.ll[0] = ll[0];
+    e->res.ll[1] = ll[1];
+  }
   FH_CUDA(cudaMemcpyAsync(&e->io_flag[slot], e->flag.p, sizeof(FailFlag), cudaMemcpyDeviceToHost, e->stream));
   FH_CUDA(cudaStreamWaitEvent(e->stream, ev[3], 0));
   current_T_to_stage(e, e->io_out[slot].p);

@@ -61,10 +61,6 @@ constexpr int kMinBlocksTetF64 = 3;
 #ifndef FH_NODE_UNROLL_TET
 #define FH_NODE_UNROLL_TET 1
 #endif
-// LEAN loops: batch records pulled into L2 this many batches ahead of the ring (0: off)
-#ifndef FH_LEAN_PF
-#define FH_LEAN_PF 0
-#endif
 // per-tile material / single-RF node bodies (0: the general body whenever node regions exist)
 #ifndef FH_PART_MAT
 #define FH_PART_MAT 1
@@ -306,13 +302,6 @@ __device__ __forceinline__ void lean_issue(const TiledArgs<S> &g, int s_start, i
   mbar_expect_tx(bar, (uint32_t)(RecBytes<S>(N) + (N == 4 ? kBatch : 0)));
   bulk_g2s(stage, rec, RecBytes<S>(N), bar);
   if (N == 4) bulk_g2s(stage + RecBytes<S>(N), g.tet_phase + s_start + j * kBatch, kBatch, bar);
-}
-
-// L2 prefetch of the record of batch j (LEAN loops, FH_LEAN_PF batches ahead of the ring)
-template <typename S, int N>
-__device__ __forceinline__ void lean_prefetch(const TiledArgs<S> &g, int s_start, int j) {
-  const unsigned char *rec = (N == 4 ? g.tet_rec : g.hex_rec) + (size_t)(s_start / kBatch + j) * RecBytes<S>(N);
-  bulk_prefetch_l2(rec, (uint32_t)RecBytes<S>(N));
 }
 
 // LEAN 3 (mixed tiles): batch j of the tile is a tet batch while j < nbt, then a hex batch
@@ -608,10 +597,6 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
       else
         issue_batch(g, p, j, nbt, ring + j * g.stage_bytes, &bars[j], preg < 0);
     }
-    if constexpr (LEAN != 0 && FH_LEAN_PF > 0 && KINDS != 2) {
-      for (int j = kStages; j < kStages + FH_LEAN_PF && j < nb; ++j)
-        lean_prefetch<S, KINDS == 1 ? 4 : 8>(g, KINDS == 1 ? t_start : h_start, j);
-    }
 #if FH_PREFETCH_NODES
     // the node update's per-node streams, pulled into L2 while the batches run
     if (g.n_src) prefetch_range(g.xyzv + 4 * (size_t)n0, 4 * sizeof(S) * nfree);
@@ -744,10 +729,6 @@ __global__ void __launch_bounds__(kTileThreads, sizeof(S) == 4 ? (KINDS == 1 ? k
           fence_proxy_async();
           if constexpr (KINDS == 2) lean_issue_mixed<S>(g, t_start, h_start, nbt, j + kStages, stage, &bars[st]);
           else lean_issue<S, KINDS == 1 ? 4 : 8>(g, KINDS == 1 ? t_start : h_start, j + kStages, stage, &bars[st]);
-        }
-        if constexpr (FH_LEAN_PF > 0 && KINDS != 2) {
-          if (tid == 0 && j + kStages + FH_LEAN_PF < nb)
-            lean_prefetch<S, KINDS == 1 ? 4 : 8>(g, KINDS == 1 ? t_start : h_start, j + kStages + FH_LEAN_PF);
         }
       };
       // mixed tiles (LEAN 3): the tile's tet batches come first

@@ -132,3 +132,29 @@ def test_async_failure_resets_and_refuses():
     N.check(L.fh_set_temperature(h, N.ptr(Tin), Tin.size, 0, 0.0))
     N.check(L.fh_step_host_async(h, N.ptr(Tin), N.ptr(Tout), Tin.size, 1, dt / 10.0, 1))
     N.check(L.fh_host_wait(h, 1, C.byref(rep)))
+
+
+def test_async_failure_on_the_resident_exact_kernel_stops_at_the_failing_step():
+    """A multi-step asynchronous call cannot replay a runaway, so it keeps the
+    resident kernel's grid barrier: the field that comes back is the one right
+    after the failing step, exactly what the synchronous call reports."""
+    mesh, mat, T0 = unstable_problem(div=12)
+    dt = None
+    fields = []
+    for mode in ("sync", "async"):
+        eng = fh.ExplicitEngine(mesh, mat)  # EXACT fp64, resident kernel (stamped halo words by default)
+        assert eng.layout()["kernels_per_step"] == 0
+        dt = dt or 3.0 * eng.critical_dt(T0)
+        L, h = eng._L, eng._h
+        Tin = N.f64(T0)
+        Tout = np.empty_like(Tin)
+        rep = N.FhReport()
+        if mode == "sync":
+            assert L.fh_step_host(h, N.ptr(Tin), N.ptr(Tout), Tin.size, 300, dt, C.byref(rep)) == 2
+        else:
+            N.check(L.fh_set_temperature(h, N.ptr(Tin), Tin.size, 0, 0.0))
+            N.check(L.fh_step_host_async(h, N.ptr(Tin), N.ptr(Tout), Tin.size, 300, dt, 0))
+            assert L.fh_host_wait(h, 0, C.byref(rep)) == 2
+        fields.append((rep.fail_step, eng.temperature()))
+    assert fields[0][0] == fields[1][0] > 1
+    assert np.array_equal(fields[0][1], fields[1][1], equal_nan=True)

@@ -691,7 +691,11 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   }
   // mixed meshes: inside each launch range the tiles holding tets come first,
   // so the hex-only tiles can run the leaner hex-only kernel instance
+  const bool has_regions = o.n_materials > 1 && o.element_region;
   bool split = e->n_tet > 0 && e->n_hex > 0;
+  // a hex-only mesh with material regions splits the same way on one GPU (no
+  // tile holds tets), so that its region-0 tiles can run the LEAN 2 loop below
+  if (e->n_tet == 0 && e->n_hex > 0 && has_regions && e->X.world == 1) split = true;
   if (o.kind_split == 1) split = false;
   st->n_mixed_b = st->n_boundary;
   st->n_mixed_i = st->n_parts_local - st->n_boundary;
@@ -706,7 +710,6 @@ void setup_tiled(fh_engine *e, const fh_mesh &mesh, const fh_boundary &b, const 
   // hex-only tiles whose slots all lie in region 0 go last and run the LEAN 2
   // loop (fh_tiled.cu); the region-0 tiles that hold tets go to the end of the
   // mixed range and run the LEAN 3 loop; the others keep the general kernel
-  const bool has_regions = o.n_materials > 1 && o.element_region;
   if (e->X.world == 1 && (has_regions || split) && e->td && o.lean_kernels == 0 && o.tile_mode == 0 &&
       P.corner_unique && sizeof(S) == 4 && !(e->kfactor.p && !e->td)) {
     MatSet<S> mt = mats_of<S>(e);

@@ -1222,7 +1222,11 @@ void tiled_run(fh_engine *e, int64_t nsteps, double dt) {
       // the two instances run concurrently (disjoint tiles): the mixed tiles
       // on a side stream, so their last wave overlaps the hex-only tiles
       if (!e->kind_stream) {
-        FH_CUDA(cudaStreamCreateWithFlags(&e->kind_stream, cudaStreamNonBlocking));
+        // highest priority: the side stream's few tiles are placed as SM slots free up, ahead of
+        // the engine stream's many, so the step ends on the big launch's full-occupancy tail
+        int prio_lo = 0, prio_hi = 0;
+        FH_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        FH_CUDA(cudaStreamCreateWithPriority(&e->kind_stream, cudaStreamNonBlocking, prio_hi));
         FH_CUDA(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
         FH_CUDA(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
       }
